@@ -1,0 +1,174 @@
+"""CPU ORACLE binding — TEST INFRASTRUCTURE ONLY.
+
+ctypes wrapper over ``oracle/librgf_oracle.so``, the Eigen-free C++
+restatement of the reference hot path (see rgf_oracle.h). Imported only by
+tests/, ``__graft_entry__.smoke()`` and bench.py's CPU-baseline legs, as the
+checker or the timed CPU baseline; the product package never imports it.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librgf_oracle.so")
+
+
+def build(force: bool = False) -> str:
+    if force or not os.path.exists(LIB_PATH):
+        subprocess.check_call(["make", "-s", "-C", _HERE])
+    return LIB_PATH
+
+
+build()
+lib = ctypes.CDLL(LIB_PATH)
+
+_vp = ctypes.c_void_p
+_i64 = ctypes.c_int64
+_d = ctypes.c_double
+lib.rgfo_last_error.restype = ctypes.c_char_p
+lib.rgfo_rf3_coefficients.argtypes = [_d, _vp]
+lib.rgfo_rf3_filter_scalars.argtypes = [_d, ctypes.c_int, _vp]
+lib.rgfo_rf3_cascade_variance.argtypes = [_d]
+lib.rgfo_rf3_cascade_variance.restype = _d
+lib.rgfo_rf3_length_scale_argument.argtypes = [_d, ctypes.c_int]
+lib.rgfo_rf3_length_scale_argument.restype = _d
+lib.rgfo_rf1_coefficients.argtypes = [_d, ctypes.c_int, _vp]
+lib.rgfo_rational_gauss.argtypes = [_d]
+lib.rgfo_rational_gauss.restype = _d
+lib.rgfo_rf3_apply_1d.argtypes = [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp]
+lib.rgfo_rf1_apply_1d.argtypes = [_vp, _vp, _i64, ctypes.c_int, ctypes.c_int, _vp]
+lib.rgfo_rf3_apply_1d_coeffs.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, ctypes.c_int, _vp]
+lib.rgfo_op_create.argtypes = [_i64, _i64, _i64, _vp, _vp, _vp, _i64, _vp, _vp, ctypes.c_int,
+                               ctypes.c_int, ctypes.c_int, _i64, _vp, ctypes.c_int,
+                               ctypes.c_int, ctypes.POINTER(_vp)]
+lib.rgfo_op_destroy.argtypes = [_vp]
+lib.rgfo_op_apply.argtypes = [_vp, ctypes.c_int, _vp, _vp, _i64, _i64, _i64]
+lib.rgfo_op_ghost_width.argtypes = [_vp, _i64]
+lib.rgfo_op_ghost_width.restype = _i64
+lib.rgfo_op_coefficient_bytes.argtypes = [_vp]
+lib.rgfo_op_coefficient_bytes.restype = ctypes.c_uint64
+lib.rgfo_op_uniform.argtypes = [_vp, _i64, ctypes.c_int]
+lib.rgfo_resolve_thread_count.argtypes = [ctypes.c_int]
+
+GX, GY, GXT, GYT, V, VT, B, GYGX = range(8)
+
+
+class OracleError(ValueError):
+    pass
+
+
+def _check(status):
+    if status != 0:
+        raise OracleError(lib.rgfo_last_error().decode())
+
+
+def _p(a):
+    return a.ctypes.data
+
+
+def rf3_coefficients(sigma):
+    out = np.zeros(8)
+    _check(lib.rgfo_rf3_coefficients(float(sigma), _p(out)))
+    return out  # a0 a1 a2 a3 alpha1 alpha2 alpha3 beta
+
+
+def rf3_filter_scalars(sigma, calibration=0):
+    out = np.zeros(5)
+    _check(lib.rgfo_rf3_filter_scalars(float(sigma), int(calibration), _p(out)))
+    return out  # alpha1 alpha2 alpha3 beta q
+
+
+def rf1_coefficients(sigma, k):
+    out = np.zeros(2)
+    _check(lib.rgfo_rf1_coefficients(float(sigma), int(k), _p(out)))
+    return out
+
+
+def rf3_cascade_variance(q):
+    return lib.rgfo_rf3_cascade_variance(float(q))
+
+
+def rf3_length_scale_argument(sigma, calibration):
+    return lib.rgfo_rf3_length_scale_argument(float(sigma), int(calibration))
+
+
+def rational_gauss(t):
+    return lib.rgfo_rational_gauss(float(t))
+
+
+def rf3_apply_1d(x, sigma, calibration=0, transpose=False):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    sig = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma, dtype=np.float64), x.shape))
+    out = np.empty_like(x)
+    _check(lib.rgfo_rf3_apply_1d(_p(x), _p(sig), x.size, int(calibration), int(transpose),
+                                 _p(out)))
+    return out
+
+
+def rf1_apply_1d(x, sigma, k, transpose=False):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    sig = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma, dtype=np.float64), x.shape))
+    out = np.empty_like(x)
+    _check(lib.rgfo_rf1_apply_1d(_p(x), _p(sig), x.size, int(k), int(transpose), _p(out)))
+    return out
+
+
+def rf3_apply_1d_coeffs(x, a1, a2, a3, b, transpose=False):
+    arrs = [np.ascontiguousarray(v, dtype=np.float64) for v in (x, a1, a2, a3, b)]
+    out = np.empty_like(arrs[0])
+    _check(lib.rgfo_rf3_apply_1d_coeffs(*(_p(v) for v in arrs), arrs[0].size, int(transpose),
+                                        _p(out)))
+    return out
+
+
+class OracleOp:
+    """Loop of per-level 2-D HorizontalCovarianceOp instances (CPU)."""
+
+    def __init__(self, nx, ny, dx, dy, mask, rx, ry, order=3, k_iterations=1, unit_dc=True,
+                 ghost_width=None, grid_ghost_width=0, variance=None, threads=1,
+                 calibration=0):
+        self.nx, self.ny = int(nx), int(ny)
+        mask = np.asarray(mask)
+        self.nlev = 1 if mask.ndim == 2 else mask.shape[0]
+        self._keep = [np.ascontiguousarray(a, dtype=np.float64) for a in (dx, dy, rx, ry)]
+        self._mask = np.ascontiguousarray(mask.reshape(self.nlev, ny, nx), dtype=np.uint8)
+        var = None
+        if variance is not None:
+            var = np.ascontiguousarray(np.broadcast_to(
+                np.asarray(variance, dtype=np.float64).reshape(-1, ny, nx), (self.nlev, ny, nx)))
+            self._keep.append(var)
+        h = _vp()
+        dxa, dya, rxa, rya = self._keep[:4]
+        _check(lib.rgfo_op_create(self.nx, self.ny, self.nlev, _p(dxa), _p(dya), _p(self._mask),
+                                  int(grid_ghost_width), _p(rxa), _p(rya), int(order),
+                                  int(k_iterations), 1 if unit_dc else 0,
+                                  -1 if ghost_width is None else int(ghost_width),
+                                  None if var is None else _p(var), int(threads),
+                                  int(calibration), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.rgfo_op_destroy(self._h)
+            self._h = None
+
+    def ghost_width(self, level=0):
+        return lib.rgfo_op_ghost_width(self._h, level)
+
+    def coefficient_bytes(self):
+        return lib.rgfo_op_coefficient_bytes(self._h)
+
+    def uniform(self, level, direction):
+        return bool(lib.rgfo_op_uniform(self._h, level, direction))
+
+    def apply(self, kind, field, lev0=0, nlev_sub=0):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        planes = nlev_sub if nlev_sub > 0 else self.nlev
+        nvar = f.size // (self.nx * self.ny * planes)
+        out = np.empty_like(f)
+        _check(lib.rgfo_op_apply(self._h, kind, _p(f), _p(out), nvar, lev0, nlev_sub))
+        return out

@@ -1,0 +1,422 @@
+"""B200-native recursive-filter horizontal covariance operator (arXiv 1404.5756).
+
+Python mirror of the reference C++ interface (``rgf`` namespace of
+/root/reference/proj/include/rgf): ``Grid2D``, ``ScaleField``,
+``uniform_scale``, ``CovarianceOptions``, ``HorizontalCovarianceOp`` with the
+seven ``apply_*`` methods, ``effective_ghost_width`` and
+``coefficient_bytes``, plus the scalar coefficient builders and 1-D entry
+points. Every call goes through the C ABI in ``include/rgf_b200.h``
+(``librgf_b200.so``, sm_100a kernels). There is no CPU fallback: without the
+built library the import fails, without a GPU the calls raise.
+
+Array convention: numpy/torch arrays are C-ordered ``(ny, nx)`` per level, so
+element ``[iy, ix]`` sits at ``iy*nx + ix`` — the reference's x-fastest
+layout (types.hpp:25-28). Batched fields are ``(nvar, nlev, ny, nx)``.
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from dataclasses import dataclass, field as dc_field
+from typing import Optional
+
+import numpy as np
+
+__all__ = [
+    "FilterOrder", "Rf3Calibration", "Grid2D", "ScaleField", "uniform_scale",
+    "CovarianceOptions", "HorizontalCovarianceOp", "InvalidArgument", "DeviceError",
+    "rf3_coefficients", "rf3_filter_scalars", "rf1_coefficients",
+    "rf3_apply_1d", "rf3_apply_transpose_1d", "rf1_apply_1d", "rf1_apply_transpose_1d",
+    "lib", "LIB_PATH",
+]
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "librgf_b200.so")
+
+if not os.path.exists(LIB_PATH):  # fail loudly: the product has no fallback
+    raise ImportError(
+        f"{LIB_PATH} is missing; build it with `python -c 'import __graft_entry__ as g; g.build()'`")
+
+lib = ctypes.CDLL(LIB_PATH)
+
+_i64 = ctypes.c_int64
+_i32 = ctypes.c_int32
+_dp = ctypes.POINTER(ctypes.c_double)
+_vp = ctypes.c_void_p
+
+
+class _GridDesc(ctypes.Structure):
+    _fields_ = [("nx", _i64), ("ny", _i64), ("nlev", _i64), ("dx", _vp), ("dy", _vp),
+                ("mask", _vp), ("ghost_width", _i64)]
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("order", _i32), ("k_iterations", _i32), ("unit_dc", _i32),
+                ("calibration", _i32), ("ghost_width", _i64), ("variance", _vp),
+                ("threads", _i32), ("device", _i32)]
+
+
+lib.rgf_last_error.restype = ctypes.c_char_p
+lib.rgf_options_default.argtypes = [ctypes.POINTER(_Options)]
+lib.rgf_options_default.restype = None
+lib.rgf_op_create.argtypes = [ctypes.POINTER(_GridDesc), _vp, _vp, ctypes.POINTER(_Options),
+                              ctypes.POINTER(_vp)]
+lib.rgf_op_destroy.argtypes = [_vp]
+lib.rgf_op_apply.argtypes = [_vp, ctypes.c_int, ctypes.c_int, _vp, _vp, _i64, ctypes.c_int, _vp]
+lib.rgf_op_ghost_width.argtypes = [_vp, _i64, ctypes.POINTER(_i64)]
+lib.rgf_op_coefficient_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
+lib.rgf_op_device_bytes.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
+lib.rgf_op_launch_count.argtypes = [_vp, ctypes.POINTER(ctypes.c_uint64)]
+lib.rgf_op_segments.argtypes = [_vp, ctypes.c_int, ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                _vp, _vp]
+lib.rgf_op_coefficients.argtypes = [_vp, ctypes.c_int, _vp, _vp, _vp, _vp, _vp]
+lib.rgf_rf3_coefficients.argtypes = [ctypes.c_double, _dp]
+lib.rgf_rf3_filter_scalars.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
+lib.rgf_rf1_coefficients.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
+lib.rgf_rf3_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
+lib.rgf_rf1_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
+
+# C ABI constants (include/rgf_b200.h)
+GX, GY, GXT, GYT, V, VT, B, GYGX = range(8)
+F64, F32 = 0, 1
+HOST, DEVICE = 0, 1
+
+
+class InvalidArgument(ValueError):
+    """The reference's std::invalid_argument (same message text)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA failure (no device, launch error, out of memory)."""
+
+
+def _check(status: int) -> None:
+    if status == 0:
+        return
+    msg = lib.rgf_last_error().decode()
+    if status == 1:
+        raise InvalidArgument(msg)
+    if status == 3:
+        raise DeviceError(msg)
+    raise RuntimeError(msg)
+
+
+class FilterOrder(enum.IntEnum):  # types.hpp:30
+    first = 1
+    third = 3
+
+
+class Rf3Calibration(enum.IntEnum):  # types.hpp:39
+    yvv95 = 0
+    variance_match = 1
+    none = 2
+
+
+def _ptr(a: np.ndarray) -> int:
+    return a.ctypes.data
+
+
+@dataclass
+class Grid2D:
+    """grid.hpp:20-37, with an optional level axis on the mask.
+
+    dx, dy: (ny, nx) metres. mask: (ny, nx) or (nlev, ny, nx), True = sea.
+    """
+    nx: int
+    ny: int
+    dx: np.ndarray
+    dy: np.ndarray
+    mask: np.ndarray
+    ghost_width: int = 0
+
+    @staticmethod
+    def uniform(nx: int, ny: int, dx: float, dy: float, ghost_width: int = 0,
+                nlev: int = 1) -> "Grid2D":
+        shape = (ny, nx) if nlev == 1 else (nlev, ny, nx)
+        return Grid2D(nx, ny, np.full((ny, nx), float(dx)), np.full((ny, nx), float(dy)),
+                      np.ones(shape, dtype=bool), ghost_width)
+
+    @property
+    def nlev(self) -> int:
+        return 1 if np.ndim(self.mask) == 2 else int(np.shape(self.mask)[0])
+
+    def size(self) -> int:
+        return self.nx * self.ny
+
+    def all_sea(self) -> bool:
+        return bool(np.all(self.mask))
+
+
+@dataclass
+class ScaleField:
+    """grid.hpp:40-52: per-point correlation radii (metres), (ny, nx)."""
+    rx: np.ndarray
+    ry: np.ndarray
+
+    def sigma_x(self, grid: Grid2D) -> np.ndarray:  # grid.cpp:57-59 (2-D grids)
+        return np.where(grid.mask, self.rx / grid.dx, 1.0)
+
+    def sigma_y(self, grid: Grid2D) -> np.ndarray:
+        return np.where(grid.mask, self.ry / grid.dy, 1.0)
+
+
+def uniform_scale(grid: Grid2D, r: float) -> ScaleField:
+    """grid.cpp:69-76."""
+    if not r > 0:
+        raise InvalidArgument("uniform_scale: radius must be positive")
+    return ScaleField(np.full((grid.ny, grid.nx), float(r)), np.full((grid.ny, grid.nx), float(r)))
+
+
+@dataclass
+class CovarianceOptions:
+    """covariance.hpp:17-25 (plus the CUDA device ordinal)."""
+    order: FilterOrder = FilterOrder.third
+    k_iterations: int = 1
+    unit_dc: bool = True
+    ghost_width: Optional[int] = None
+    variance: Optional[np.ndarray] = None
+    threads: int = 0
+    calibration: Rf3Calibration = Rf3Calibration.yvv95
+    device: int = 0
+
+
+class HorizontalCovarianceOp:
+    """covariance.hpp:35-79: V_H = G_y G_x on a masked grid and its relatives.
+
+    apply_* accept numpy arrays (host: copied to the device and back, like
+    the reference's out-of-place StateField returns) or CUDA torch tensors
+    (device-resident, asynchronous on the current stream).
+    """
+
+    def __init__(self, grid: Grid2D, scales: ScaleField,
+                 options: Optional[CovarianceOptions] = None):
+        options = options or CovarianceOptions()
+        self.grid_ = grid
+        self.options_ = options
+        nx, ny, nlev = int(grid.nx), int(grid.ny), grid.nlev
+        shape_ok = (np.shape(grid.dx) == (ny, nx) and np.shape(grid.dy) == (ny, nx))
+        if not shape_ok:
+            raise InvalidArgument("Grid2D: spacing field shape mismatch")
+        if np.shape(grid.mask)[-2:] != (ny, nx):
+            raise InvalidArgument("Grid2D: mask shape mismatch")
+        if np.shape(scales.rx) != (ny, nx) or np.shape(scales.ry) != (ny, nx):
+            raise InvalidArgument("ScaleField: shape does not match grid")
+        self._dx = np.ascontiguousarray(grid.dx, dtype=np.float64)
+        self._dy = np.ascontiguousarray(grid.dy, dtype=np.float64)
+        self._mask = np.ascontiguousarray(np.reshape(grid.mask, (nlev, ny, nx)), dtype=np.uint8)
+        self._rx = np.ascontiguousarray(scales.rx, dtype=np.float64)
+        self._ry = np.ascontiguousarray(scales.ry, dtype=np.float64)
+        desc = _GridDesc(nx, ny, nlev, _ptr(self._dx), _ptr(self._dy), _ptr(self._mask),
+                         int(grid.ghost_width))
+        opt = _Options()
+        lib.rgf_options_default(ctypes.byref(opt))
+        opt.order = int(options.order)
+        opt.k_iterations = int(options.k_iterations)
+        opt.unit_dc = 1 if options.unit_dc else 0
+        opt.calibration = int(options.calibration)
+        opt.ghost_width = -1 if options.ghost_width is None else int(options.ghost_width)
+        if options.ghost_width is not None and options.ghost_width < 0:
+            raise InvalidArgument("covariance: ghost_width < 0")
+        self._var = None
+        if options.variance is not None:
+            var = np.asarray(options.variance, dtype=np.float64)
+            if var.shape[-2:] != (ny, nx) or (var.ndim == 3 and var.shape[0] != nlev):
+                raise InvalidArgument("covariance: variance field shape mismatch")
+            self._var = np.ascontiguousarray(np.broadcast_to(var.reshape((-1, ny, nx)),
+                                                             (nlev, ny, nx)))
+            opt.variance = _ptr(self._var)
+        opt.threads = int(options.threads)
+        opt.device = int(options.device)
+        handle = _vp()
+        _check(lib.rgf_op_create(ctypes.byref(desc), _ptr(self._rx), _ptr(self._ry),
+                                 ctypes.byref(opt), ctypes.byref(handle)))
+        self._h = handle
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.rgf_op_destroy(h)
+            self._h = None
+
+    # -- reference accessors (covariance.hpp:49-56)
+    def grid(self) -> Grid2D:
+        return self.grid_
+
+    def options(self) -> CovarianceOptions:
+        return self.options_
+
+    def effective_ghost_width(self, level: int = 0) -> int:
+        out = _i64()
+        _check(lib.rgf_op_ghost_width(self._h, level, ctypes.byref(out)))
+        return out.value
+
+    def coefficient_bytes(self) -> int:
+        out = ctypes.c_uint64()
+        _check(lib.rgf_op_coefficient_bytes(self._h, ctypes.byref(out)))
+        return out.value
+
+    def device_bytes(self) -> int:
+        out = ctypes.c_uint64()
+        _check(lib.rgf_op_device_bytes(self._h, ctypes.byref(out)))
+        return out.value
+
+    def launch_count(self) -> int:
+        out = ctypes.c_uint64()
+        _check(lib.rgf_op_launch_count(self._h, ctypes.byref(out)))
+        return out.value
+
+    def segments(self, direction: int):
+        """(offsets[nlines+1], segs[nsegs, 2]) built by the segmentation kernel."""
+        nl, ns = _i64(), _i64()
+        _check(lib.rgf_op_segments(self._h, direction, ctypes.byref(nl), ctypes.byref(ns),
+                                   None, None))
+        off = np.empty(nl.value + 1, dtype=np.int64)
+        segs = np.empty((max(ns.value, 1), 2), dtype=np.int32)
+        _check(lib.rgf_op_segments(self._h, direction, None, None, _ptr(off), _ptr(segs)))
+        return off, segs[: ns.value]
+
+    def coefficients(self, direction: int) -> dict:
+        nh = self.grid_.nx * self.grid_.ny
+        shp = (self.grid_.ny, self.grid_.nx)
+        out = {k: np.zeros(shp) for k in ("alpha1", "alpha2", "alpha3", "beta", "inv_dc")}
+        _check(lib.rgf_op_coefficients(self._h, direction, *(_ptr(out[k]) for k in
+                                       ("alpha1", "alpha2", "alpha3", "beta", "inv_dc"))))
+        del nh
+        return out
+
+    # -- applies (covariance.cpp:362-398)
+    def apply(self, kind: int, field, out=None, stream=None):
+        """Generic entry: kind in {GX, GY, GXT, GYT, V, VT, B, GYGX}."""
+        try:
+            import torch  # plumbing only
+            is_torch = isinstance(field, torch.Tensor)
+        except ImportError:  # pragma: no cover
+            is_torch = False
+        nx, ny, nlev = self.grid_.nx, self.grid_.ny, self.grid_.nlev
+        if is_torch:
+            return self._apply_torch(kind, field, out, stream)
+        f = np.asarray(field)
+        if f.dtype not in (np.float64, np.float32):
+            f = f.astype(np.float64)
+        if f.shape[-2:] != (ny, nx) or f.size % (nx * ny * nlev) != 0:
+            raise InvalidArgument("apply: field is not on the expected grid")
+        f = np.ascontiguousarray(f)
+        nvar = f.size // (nx * ny * nlev)
+        res = np.empty_like(f) if out is None else out
+        dtype = F64 if f.dtype == np.float64 else F32
+        _check(lib.rgf_op_apply(self._h, kind, dtype, _ptr(f), _ptr(res), nvar, HOST, None))
+        return res
+
+    def _apply_torch(self, kind, field, out, stream):
+        import torch
+        nx, ny, nlev = self.grid_.nx, self.grid_.ny, self.grid_.nlev
+        if not field.is_cuda:
+            raise InvalidArgument("apply: torch tensors must be on the CUDA device")
+        if field.dtype not in (torch.float64, torch.float32) or not field.is_contiguous():
+            raise InvalidArgument("apply: expected a contiguous float64/float32 tensor")
+        if tuple(field.shape[-2:]) != (ny, nx) or field.numel() % (nx * ny * nlev):
+            raise InvalidArgument("apply: field is not on the expected grid")
+        nvar = field.numel() // (nx * ny * nlev)
+        res = torch.empty_like(field) if out is None else out
+        dtype = F64 if field.dtype == torch.float64 else F32
+        st = stream if stream is not None else torch.cuda.current_stream(field.device)
+        _check(lib.rgf_op_apply(self._h, kind, dtype, field.data_ptr(), res.data_ptr(), nvar,
+                                DEVICE, st.cuda_stream))
+        return res
+
+    def apply_gx(self, f):
+        return self.apply(GX, f)
+
+    def apply_gy(self, f):
+        return self.apply(GY, f)
+
+    def apply_gx_transpose(self, f):
+        return self.apply(GXT, f)
+
+    def apply_gy_transpose(self, f):
+        return self.apply(GYT, f)
+
+    def apply_v(self, f):
+        return self.apply(V, f)
+
+    def apply_v_transpose(self, f):
+        return self.apply(VT, f)
+
+    def apply_b(self, f):
+        return self.apply(B, f)
+
+
+# ---------------------------------------------------------------- scalars
+@dataclass
+class Rf3PolynomialSet:  # rf3.hpp:71-76
+    a0: float
+    a1: float
+    a2: float
+    a3: float
+    alpha1: float
+    alpha2: float
+    alpha3: float
+    beta: float
+
+
+@dataclass
+class Rf3Scalars:  # rf3.hpp:159-164
+    alpha1: float
+    alpha2: float
+    alpha3: float
+    beta: float
+    q: float
+
+
+@dataclass
+class Rf1Scalars:  # rf1.hpp:403-407
+    alpha: float
+    beta: float
+
+
+def rf3_coefficients(sigma: float) -> Rf3PolynomialSet:
+    out = (ctypes.c_double * 8)()
+    _check(lib.rgf_rf3_coefficients(float(sigma), out))
+    return Rf3PolynomialSet(*out)
+
+
+def rf3_filter_scalars(sigma: float, calibration: Rf3Calibration = Rf3Calibration.yvv95
+                       ) -> Rf3Scalars:
+    out = (ctypes.c_double * 5)()
+    _check(lib.rgf_rf3_filter_scalars(float(sigma), int(calibration), out))
+    return Rf3Scalars(*out)
+
+
+def rf1_coefficients(sigma: float, k: int) -> Rf1Scalars:
+    out = (ctypes.c_double * 2)()
+    _check(lib.rgf_rf1_coefficients(float(sigma), int(k), out))
+    return Rf1Scalars(*out)
+
+
+def _apply_1d(fn, x, sigma, *args):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    m = x.shape[-1]
+    sig = np.ascontiguousarray(np.broadcast_to(np.asarray(sigma, dtype=np.float64), (m,)))
+    out = np.empty_like(x)
+    nlines = x.size // m if m else 0
+    _check(fn(_ptr(x), _ptr(sig), m, max(nlines, 1), *args, _ptr(out)))
+    return out
+
+
+def rf3_apply_1d(x, sigma, calibration=Rf3Calibration.yvv95):
+    """rf3.hpp:318-325 with rf3_filter_coefficients(sigma) (rf3.hpp:191-210)."""
+    return _apply_1d(lib.rgf_rf3_apply_1d, x, sigma, int(calibration), 0)
+
+
+def rf3_apply_transpose_1d(x, sigma, calibration=Rf3Calibration.yvv95):
+    return _apply_1d(lib.rgf_rf3_apply_1d, x, sigma, int(calibration), 1)
+
+
+def rf1_apply_1d(x, sigma, k):
+    """rf1.hpp:475-482 with rf1_coefficients(sigma, k) (rf1.hpp:432-446)."""
+    return _apply_1d(lib.rgf_rf1_apply_1d, x, sigma, int(k), 0)
+
+
+def rf1_apply_transpose_1d(x, sigma, k):
+    return _apply_1d(lib.rgf_rf1_apply_1d, x, sigma, int(k), 1)

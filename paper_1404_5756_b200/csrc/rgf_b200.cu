@@ -1,0 +1,639 @@
+// C ABI of the B200-native covariance operator (include/rgf_b200.h).
+//
+// Host side of the drop-in boundary: HorizontalCovarianceOp construction
+// (covariance.cpp:155-220) becomes validation + coefficient precompute +
+// segmentation kernels; the seven apply_* methods (covariance.cpp:362-398)
+// become sequences of sweep kernels on one CUDA stream. No CPU arithmetic
+// touches field values.
+#include <cub/device/device_scan.cuh>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/rgf_b200.h"
+#include "common.cuh"
+#include "setup_kernels.cuh"
+#include "sweep_generic.cuh"
+#include "sweep_stream.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define CUDA_OK(expr)                                                                  \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      throw CudaError(std::string("CUDA error ") + cudaGetErrorString(e_) + " at " +   \
+                      __FILE__ + ":" + std::to_string(__LINE__) + " (" #expr ")");   \
+  } while (0)
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return RGF_OK;
+  } catch (const CudaError& e) {
+    g_last_error = e.what();
+    return RGF_ECUDA;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return RGF_EINVAL;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RGF_ERUNTIME;
+  }
+}
+
+template <typename T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count <= n && p) return;
+    release();
+    if (count == 0) return;
+    CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* h, size_t count) {
+    alloc(count);
+    CUDA_OK(cudaMemcpy(p, h, count * sizeof(T), cudaMemcpyHostToDevice));
+  }
+  size_t bytes() const { return n * sizeof(T); }
+};
+
+int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
+  int64_t b = (work + threads - 1) / threads;
+  if (b < 1) b = 1;
+  if (b > max_blocks) b = max_blocks;
+  return static_cast<int>(b);
+}
+
+struct DirData {
+  DevBuf<rgfb::Coef3> c3;
+  DevBuf<double2> c1;
+  DevBuf<double> idc;
+  DevBuf<int64_t> seg_off;  // nlev*lines + 1
+  DevBuf<int2> segs;
+  int64_t nsegs = 0;
+  std::vector<char> uniform;        // per level
+  std::vector<double> sigma_u;      // per level, uniform sigma value
+};
+
+}  // namespace
+
+struct rgf_op {
+  int device = 0;
+  int64_t nx = 0, ny = 0, nlev = 0;
+  int order = 3, k = 1, unit_dc = 1, calibration = 0;
+  std::vector<int64_t> ghost;  // per level
+  int64_t gmax = 0;
+  DevBuf<int> ghost_d;
+  DirData dx_, dy_;
+  DevBuf<double> variance;
+  bool has_variance = false;
+  // apply-time buffers (grown on demand)
+  DevBuf<char> in_d, out_d, tmp1, tmp2;
+  DevBuf<double> scratch;
+  int64_t scratch_threads = 0, scratch_slab = 0;
+  cudaStream_t own_stream = nullptr;
+  unsigned long long launches = 0;
+  std::mutex mu;  // apply() is const in the reference; serialize buffer reuse
+
+  ~rgf_op() {
+    if (own_stream) cudaStreamDestroy(own_stream);
+  }
+};
+
+namespace {
+
+// ------------------------------------------------------------- sweeps
+// One directional sweep over every (var, level, line): out = G_dir in (or
+// its transpose), with optional fused per-point input/output scaling
+// (the variance multiplies of apply_v / apply_v_transpose).
+template <typename T>
+void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nvar,
+           const double* pre, const double* post, cudaStream_t st) {
+  const DirData& d = dir == 0 ? op->dx_ : op->dy_;
+  const int64_t lines = nvar * op->nlev * (dir == 0 ? op->ny : op->nx);
+
+  if (op->order == 3 && rgfb::stream_supported(op->nx, op->ny)) {
+    rgfb::StreamArgs a{};
+    a.dir = dir;
+    a.transpose = transpose;
+    a.unit_dc = op->unit_dc;
+    a.nx = op->nx;
+    a.ny = op->ny;
+    a.nlev = op->nlev;
+    a.nvar = nvar;
+    a.c3 = d.c3.p;
+    a.idc = d.idc.p;
+    a.seg_off = d.seg_off.p;
+    a.segs = d.segs.p;
+    a.ghost = op->ghost_d.p;
+    a.pre_scale = pre;
+    a.post_scale = post;
+    op->launches += rgfb::launch_stream_sweep<T>(in, out, a, st);
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
+
+  const int64_t n = dir == 0 ? op->nx : op->ny;
+  const int64_t slab = n + 2 * op->gmax + 4;
+  const int threads = 128;
+  int64_t want = std::min<int64_t>(lines, 148 * 4 * threads);
+  if (op->scratch_threads < want || op->scratch_slab < slab) {
+    op->scratch_threads = std::max(op->scratch_threads, want);
+    op->scratch_slab = std::max(op->scratch_slab, slab);
+    op->scratch.alloc(static_cast<size_t>(op->scratch_threads * op->scratch_slab));
+  }
+  rgfb::SweepArgs a{};
+  a.dir = dir;
+  a.transpose = transpose;
+  a.order = op->order;
+  a.k = op->k;
+  a.unit_dc = op->unit_dc;
+  a.nx = op->nx;
+  a.ny = op->ny;
+  a.nlev = op->nlev;
+  a.nvar = nvar;
+  a.c3 = d.c3.p;
+  a.c1 = d.c1.p;
+  a.idc = d.idc.p;
+  a.seg_off = d.seg_off.p;
+  a.segs = d.segs.p;
+  a.ghost = op->ghost_d.p;
+  a.pre_scale = pre;
+  a.post_scale = post;
+  a.scratch = op->scratch.p;
+  a.slab = op->scratch_slab;
+  const int blocks = static_cast<int>((want + threads - 1) / threads);
+  rgfb::k_sweep_generic<T><<<blocks, threads, 0, st>>>(in, out, a);
+  CUDA_OK(cudaGetLastError());
+  op->launches += 1;
+}
+
+template <typename T>
+void apply_typed(rgf_op* op, int kind, const T* in, T* out, int64_t nvar, cudaStream_t st) {
+  const size_t count = static_cast<size_t>(nvar * op->nlev * op->nx * op->ny);
+  const double* var = op->has_variance ? op->variance.p : nullptr;
+  auto tmp = [&](DevBuf<char>& b) {
+    b.alloc(count * sizeof(T));
+    return reinterpret_cast<T*>(b.p);
+  };
+  switch (kind) {
+    case RGF_GX: sweep<T>(op, 0, false, in, out, nvar, nullptr, nullptr, st); break;
+    case RGF_GY: sweep<T>(op, 1, false, in, out, nvar, nullptr, nullptr, st); break;
+    case RGF_GXT: sweep<T>(op, 0, true, in, out, nvar, nullptr, nullptr, st); break;
+    case RGF_GYT: sweep<T>(op, 1, true, in, out, nvar, nullptr, nullptr, st); break;
+    case RGF_GYGX: {
+      T* t = tmp(op->tmp1);
+      sweep<T>(op, 0, false, in, t, nvar, nullptr, nullptr, st);
+      sweep<T>(op, 1, false, t, out, nvar, nullptr, nullptr, st);
+      break;
+    }
+    case RGF_V: {  // covariance.cpp:382-387: diag(var) G_y G_x
+      T* t = tmp(op->tmp1);
+      sweep<T>(op, 0, false, in, t, nvar, nullptr, nullptr, st);
+      sweep<T>(op, 1, false, t, out, nvar, nullptr, var, st);
+      break;
+    }
+    case RGF_VT: {  // covariance.cpp:389-394: G_x^T G_y^T diag(var)
+      T* t = tmp(op->tmp1);
+      sweep<T>(op, 1, true, in, t, nvar, var, nullptr, st);
+      sweep<T>(op, 0, true, t, out, nvar, nullptr, nullptr, st);
+      break;
+    }
+    case RGF_B: {  // covariance.cpp:396-398: V V^T
+      T* t = tmp(op->tmp1);
+      T* u = tmp(op->tmp2);
+      sweep<T>(op, 1, true, in, t, nvar, var, nullptr, st);
+      sweep<T>(op, 0, true, t, u, nvar, nullptr, nullptr, st);
+      sweep<T>(op, 0, false, u, t, nvar, nullptr, nullptr, st);
+      sweep<T>(op, 1, false, t, out, nvar, nullptr, var, st);
+      break;
+    }
+    default: throw InvalidArgument("apply: unknown operator kind");
+  }
+}
+
+unsigned long long read_u64(const unsigned long long* d) {
+  unsigned long long h = 0;
+  CUDA_OK(cudaMemcpy(&h, d, sizeof(h), cudaMemcpyDeviceToHost));
+  return h;
+}
+
+void build_segments(rgf_op* op, const uint8_t* mask_d, int dir, DirData& d) {
+  const int64_t lines = op->nlev * (dir == 0 ? op->ny : op->nx);
+  DevBuf<int64_t> counts;
+  counts.alloc(lines);
+  d.seg_off.alloc(lines + 1);
+  rgfb::k_seg_count<<<grid_for(lines, 128), 128>>>(mask_d, dir, op->nx, op->ny, lines,
+                                                   counts.p);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemset(d.seg_off.p, 0, sizeof(int64_t)));
+  size_t tmp_bytes = 0;
+  CUDA_OK(cub::DeviceScan::InclusiveSum(nullptr, tmp_bytes, counts.p, d.seg_off.p + 1, lines));
+  DevBuf<char> tmp;
+  tmp.alloc(tmp_bytes);
+  CUDA_OK(cub::DeviceScan::InclusiveSum(tmp.p, tmp_bytes, counts.p, d.seg_off.p + 1, lines));
+  int64_t total = 0;
+  CUDA_OK(cudaMemcpy(&total, d.seg_off.p + lines, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  d.nsegs = total;
+  d.segs.alloc(std::max<int64_t>(total, 1));
+  rgfb::k_seg_fill<<<grid_for(lines, 128), 128>>>(mask_d, dir, op->nx, op->ny, lines,
+                                                  d.seg_off.p, d.segs.p);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaDeviceSynchronize());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* rgf_last_error(void) { return g_last_error.c_str(); }
+
+void rgf_options_default(rgf_options* o) {
+  o->order = RGF_ORDER_THIRD;
+  o->k_iterations = 1;
+  o->unit_dc = 1;
+  o->calibration = RGF_CAL_YVV95;
+  o->ghost_width = -1;
+  o->variance = nullptr;
+  o->threads = 0;
+  o->device = 0;
+}
+
+int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
+                  const rgf_options* opt, rgf_op** out) {
+  if (out) *out = nullptr;
+  return guarded([&] {
+    if (!g || !rx || !ry || !opt || !out) throw InvalidArgument("rgf_op_create: null argument");
+    // grid.cpp:27-39 Grid2D::validate
+    if (g->nx < 4 || g->ny < 4) throw InvalidArgument("Grid2D: nx and ny must both be >= 4");
+    if (g->nlev < 1) throw InvalidArgument("Grid2D: nlev must be >= 1");
+    if (!g->dx || !g->dy || !g->mask) throw InvalidArgument("Grid2D: spacing field shape mismatch");
+    if (g->ghost_width < 0) throw InvalidArgument("Grid2D: ghost_width must be >= 0");
+    // covariance.cpp:159-166 option checks (after the grid/scale checks below
+    // in the reference; both orders raise invalid_argument)
+    if (opt->order != RGF_ORDER_FIRST && opt->order != RGF_ORDER_THIRD)
+      throw InvalidArgument("covariance: order must be 1 or 3");
+
+    auto op = std::make_unique<rgf_op>();
+    op->device = opt->device;
+    CUDA_OK(cudaSetDevice(op->device));
+    op->nx = g->nx;
+    op->ny = g->ny;
+    op->nlev = g->nlev;
+    const int64_t nh = g->nx * g->ny;
+
+    DevBuf<double> dx, dy, rxd, ryd;
+    DevBuf<uint8_t> mask, any_sea;
+    DevBuf<unsigned long long> flag;
+    dx.upload(g->dx, nh);
+    dy.upload(g->dy, nh);
+    rxd.upload(rx, nh);
+    ryd.upload(ry, nh);
+    mask.upload(g->mask, static_cast<size_t>(nh * g->nlev));
+    any_sea.alloc(nh);
+    flag.alloc(1);
+
+    // grid.cpp:33-34
+    CUDA_OK(cudaMemset(flag.p, 0xff, sizeof(unsigned long long)));
+    rgfb::k_check_spacing<<<grid_for(nh, 256), 256>>>(dx.p, dy.p, nh, flag.p);
+    CUDA_OK(cudaGetLastError());
+    if (read_u64(flag.p) != ~0ull)
+      throw InvalidArgument("Grid2D: grid spacing must be strictly positive");
+    // grid.cpp:41-55
+    CUDA_OK(cudaMemset(flag.p, 0xff, sizeof(unsigned long long)));
+    rgfb::k_check_scales<<<grid_for(nh, 256), 256>>>(rxd.p, ryd.p, dx.p, dy.p, mask.p, nh,
+                                                     g->nlev, flag.p, any_sea.p);
+    CUDA_OK(cudaGetLastError());
+    const unsigned long long bad = read_u64(flag.p);
+    if (bad != ~0ull) {
+      const int64_t p = static_cast<int64_t>(bad % nh);
+      throw InvalidArgument("ScaleField: non-positive or non-finite radius at sea point (" +
+                            std::to_string(p % g->nx) + "," + std::to_string(p / g->nx) + ")");
+    }
+    // covariance.cpp:159-166
+    if (opt->order == RGF_ORDER_FIRST && opt->k_iterations < 1)
+      throw InvalidArgument("covariance: k_iterations must be >= 1");
+    if (opt->order == RGF_ORDER_THIRD && opt->k_iterations != 1)
+      throw InvalidArgument("covariance: the third-order filter is single-iteration by construction");
+    if (opt->calibration < 0 || opt->calibration > 2)
+      throw InvalidArgument("covariance: unknown calibration");
+    op->order = opt->order;
+    op->k = opt->k_iterations;
+    op->unit_dc = opt->unit_dc ? 1 : 0;
+    op->calibration = opt->calibration;
+
+    // per-level sigma statistics: uniform test and max sigma
+    DevBuf<unsigned long long> stats;
+    stats.alloc(4 * g->nlev);
+    std::vector<unsigned long long> init(4 * g->nlev);
+    for (int64_t l = 0; l < g->nlev; ++l) {
+      init[4 * l + 0] = ~0ull;
+      init[4 * l + 1] = 0;
+      init[4 * l + 2] = ~0ull;
+      init[4 * l + 3] = 0;
+    }
+    CUDA_OK(cudaMemcpy(stats.p, init.data(), init.size() * 8, cudaMemcpyHostToDevice));
+    {
+      dim3 grid(grid_for(nh, 256, 256), static_cast<unsigned>(g->nlev));
+      rgfb::k_level_stats<<<grid, 256>>>(rxd.p, ryd.p, dx.p, dy.p, mask.p, nh, stats.p);
+      CUDA_OK(cudaGetLastError());
+    }
+    std::vector<unsigned long long> st(4 * g->nlev);
+    CUDA_OK(cudaMemcpy(st.data(), stats.p, st.size() * 8, cudaMemcpyDeviceToHost));
+    auto as_d = [](unsigned long long b) {
+      double v;
+      std::memcpy(&v, &b, 8);
+      return v;
+    };
+    op->ghost.resize(g->nlev);
+    op->dx_.uniform.resize(g->nlev);
+    op->dy_.uniform.resize(g->nlev);
+    op->dx_.sigma_u.resize(g->nlev);
+    op->dy_.sigma_u.resize(g->nlev);
+    for (int64_t l = 0; l < g->nlev; ++l) {
+      const double mnx = as_d(st[4 * l]), mxx = as_d(st[4 * l + 1]);
+      const double mny = as_d(st[4 * l + 2]), mxy = as_d(st[4 * l + 3]);
+      op->dx_.uniform[l] = mnx == mxx;
+      op->dy_.uniform[l] = mny == mxy;
+      op->dx_.sigma_u[l] = mnx;
+      op->dy_.sigma_u[l] = mny;
+      // covariance.cpp:173-180 ghost width resolution
+      if (opt->ghost_width >= 0) {
+        op->ghost[l] = opt->ghost_width;
+      } else if (g->ghost_width > 0) {
+        op->ghost[l] = g->ghost_width;
+      } else {
+        op->ghost[l] = static_cast<int64_t>(std::ceil(9.0 * std::max(mxx, mxy)));
+      }
+    }
+    op->gmax = *std::max_element(op->ghost.begin(), op->ghost.end());
+    std::vector<int> gi(op->ghost.begin(), op->ghost.end());
+    op->ghost_d.upload(gi.data(), gi.size());
+
+    // coefficient precompute (covariance.cpp:182-219)
+    for (int dir = 0; dir < 2; ++dir) {
+      DirData& d = dir == 0 ? op->dx_ : op->dy_;
+      const double* r = dir == 0 ? rxd.p : ryd.p;
+      const double* s = dir == 0 ? dx.p : dy.p;
+      if (op->order == 3) {
+        d.c3.alloc(nh);
+        if (op->unit_dc) d.idc.alloc(nh);
+      } else {
+        d.c1.alloc(nh);
+      }
+      const int threads = 128;
+      rgfb::k_coefficients<<<grid_for(nh, threads, 148 * 64), threads>>>(
+          r, s, any_sea.p, nh, op->order, op->k, op->calibration, op->unit_dc, d.c3.p, d.c1.p,
+          d.idc.p);
+      CUDA_OK(cudaGetLastError());
+      build_segments(op.get(), mask.p, dir, d);
+    }
+    if (opt->variance) {
+      op->variance.upload(opt->variance, static_cast<size_t>(nh * g->nlev));
+      op->has_variance = true;
+    }
+    CUDA_OK(cudaStreamCreateWithFlags(&op->own_stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaDeviceSynchronize());
+    *out = op.release();
+  });
+}
+
+int rgf_op_destroy(rgf_op* op) {
+  return guarded([&] {
+    if (!op) return;
+    cudaSetDevice(op->device);
+    delete op;
+  });
+}
+
+int rgf_op_apply(rgf_op* op, int kind, int dtype, const void* in, void* out, int64_t nvar,
+                 int memory, void* stream) {
+  return guarded([&] {
+    if (!op) throw InvalidArgument("apply: null operator");
+    if (!in || !out) throw InvalidArgument("apply: null field");
+    if (nvar < 1) throw InvalidArgument("apply: nvar must be >= 1");
+    if (dtype != RGF_F64 && dtype != RGF_F32) throw InvalidArgument("apply: unknown dtype");
+    if (kind < RGF_GX || kind > RGF_GYGX) throw InvalidArgument("apply: unknown operator kind");
+    std::lock_guard<std::mutex> lock(op->mu);
+    CUDA_OK(cudaSetDevice(op->device));
+    const size_t esz = dtype == RGF_F64 ? 8 : 4;
+    const size_t count = static_cast<size_t>(nvar * op->nlev * op->nx * op->ny);
+    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : op->own_stream;
+    const void* din = in;
+    void* dout = out;
+    if (memory == RGF_HOST) {
+      op->in_d.alloc(count * esz);
+      op->out_d.alloc(count * esz);
+      CUDA_OK(cudaMemcpyAsync(op->in_d.p, in, count * esz, cudaMemcpyHostToDevice, st));
+      din = op->in_d.p;
+      dout = op->out_d.p;
+    } else if (memory != RGF_DEVICE) {
+      throw InvalidArgument("apply: unknown memory kind");
+    }
+    if (dtype == RGF_F64)
+      apply_typed<double>(op, kind, static_cast<const double*>(din), static_cast<double*>(dout),
+                          nvar, st);
+    else
+      apply_typed<float>(op, kind, static_cast<const float*>(din), static_cast<float*>(dout),
+                         nvar, st);
+    if (memory == RGF_HOST) {
+      CUDA_OK(cudaMemcpyAsync(out, dout, count * esz, cudaMemcpyDeviceToHost, st));
+      CUDA_OK(cudaStreamSynchronize(st));
+    }
+  });
+}
+
+int rgf_op_ghost_width(const rgf_op* op, int64_t level, int64_t* out) {
+  return guarded([&] {
+    if (!op || !out) throw InvalidArgument("ghost_width: null argument");
+    if (level < 0 || level >= op->nlev) throw InvalidArgument("ghost_width: level out of range");
+    *out = op->ghost[level];
+  });
+}
+
+int rgf_op_coefficient_bytes(const rgf_op* op, uint64_t* out) {
+  return guarded([&] {
+    if (!op || !out) throw InvalidArgument("coefficient_bytes: null argument");
+    const uint64_t per_point = op->order == RGF_ORDER_FIRST ? 2 : 4;
+    *out = 2 * per_point * sizeof(double) * static_cast<uint64_t>(op->nx * op->ny);
+  });
+}
+
+int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
+  return guarded([&] {
+    if (!op || !out) throw InvalidArgument("device_bytes: null argument");
+    uint64_t b = op->ghost_d.bytes() + op->variance.bytes() + op->in_d.bytes() +
+                 op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
+    for (const DirData* d : {&op->dx_, &op->dy_})
+      b += d->c3.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes();
+    *out = b;
+  });
+}
+
+int rgf_op_launch_count(const rgf_op* op, uint64_t* out) {
+  return guarded([&] {
+    if (!op || !out) throw InvalidArgument("launch_count: null argument");
+    *out = op->launches;
+  });
+}
+
+int rgf_op_segments(const rgf_op* op, int dir, int64_t* nlines, int64_t* nsegs,
+                    int64_t* offsets, int32_t* segs) {
+  return guarded([&] {
+    if (!op) throw InvalidArgument("segments: null operator");
+    if (dir != 0 && dir != 1) throw InvalidArgument("segments: dir must be 0 or 1");
+    CUDA_OK(cudaSetDevice(op->device));
+    const DirData& d = dir == 0 ? op->dx_ : op->dy_;
+    const int64_t lines = op->nlev * (dir == 0 ? op->ny : op->nx);
+    if (nlines) *nlines = lines;
+    if (nsegs) *nsegs = d.nsegs;
+    if (offsets)
+      CUDA_OK(cudaMemcpy(offsets, d.seg_off.p, (lines + 1) * sizeof(int64_t),
+                         cudaMemcpyDeviceToHost));
+    if (segs && d.nsegs)
+      CUDA_OK(cudaMemcpy(segs, d.segs.p, d.nsegs * sizeof(int2), cudaMemcpyDeviceToHost));
+  });
+}
+
+int rgf_op_coefficients(const rgf_op* op, int dir, double* alpha1, double* alpha2,
+                        double* alpha3, double* beta, double* inv_dc) {
+  return guarded([&] {
+    if (!op) throw InvalidArgument("coefficients: null operator");
+    CUDA_OK(cudaSetDevice(op->device));
+    const DirData& d = dir == 0 ? op->dx_ : op->dy_;
+    const int64_t nh = op->nx * op->ny;
+    if (op->order == 3) {
+      std::vector<rgfb::Coef3> h(nh);
+      CUDA_OK(cudaMemcpy(h.data(), d.c3.p, nh * sizeof(rgfb::Coef3), cudaMemcpyDeviceToHost));
+      for (int64_t p = 0; p < nh; ++p) {
+        if (alpha1) alpha1[p] = h[p].a1;
+        if (alpha2) alpha2[p] = h[p].a2;
+        if (alpha3) alpha3[p] = h[p].a3;
+        if (beta) beta[p] = h[p].b;
+      }
+      if (inv_dc && op->unit_dc)
+        CUDA_OK(cudaMemcpy(inv_dc, d.idc.p, nh * sizeof(double), cudaMemcpyDeviceToHost));
+    } else {
+      std::vector<double2> h(nh);
+      CUDA_OK(cudaMemcpy(h.data(), d.c1.p, nh * sizeof(double2), cudaMemcpyDeviceToHost));
+      for (int64_t p = 0; p < nh; ++p) {
+        if (alpha1) alpha1[p] = h[p].x;
+        if (beta) beta[p] = h[p].y;
+      }
+    }
+  });
+}
+
+static void scalar_coefficients(double sigma, int calibration, int k, double* out15) {
+  DevBuf<double> d;
+  d.alloc(15);
+  CUDA_OK(cudaMemset(d.p, 0, 15 * sizeof(double)));
+  rgfb::k_scalar_coefficients<<<1, 32>>>(sigma, calibration, k, d.p);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemcpy(out15, d.p, 15 * sizeof(double), cudaMemcpyDeviceToHost));
+}
+
+int rgf_rf3_coefficients(double sigma, double out[8]) {
+  return guarded([&] {
+    if (!(sigma > 0)) throw InvalidArgument("rf3_coefficients: sigma must be positive");
+    double r[15];
+    scalar_coefficients(sigma, RGF_CAL_YVV95, 0, r);
+    std::memcpy(out, r, 8 * sizeof(double));
+  });
+}
+
+int rgf_rf3_filter_scalars(double sigma, int calibration, double out[5]) {
+  return guarded([&] {
+    if (!(sigma > 0)) throw InvalidArgument("rf3_filter_scalars: sigma must be positive");
+    if (calibration < 0 || calibration > 2) throw InvalidArgument("unknown calibration");
+    double r[15];
+    scalar_coefficients(sigma, calibration, 0, r);
+    std::memcpy(out, r + 8, 5 * sizeof(double));
+  });
+}
+
+int rgf_rf1_coefficients(double sigma, int k, double out[2]) {
+  return guarded([&] {
+    if (!(sigma > 0)) throw InvalidArgument("rf1_coefficients: sigma must be positive");
+    if (k < 1) throw InvalidArgument("rf1_coefficients: k must be >= 1");
+    double r[15];
+    scalar_coefficients(sigma, RGF_CAL_YVV95, k, r);
+    out[0] = r[13];
+    out[1] = r[14];
+  });
+}
+
+static void apply_1d(const double* in, const double* sigma, int64_t m, int64_t nlines,
+                     int order, int k, int calibration, int transpose, double* out) {
+  DevBuf<double> sig, din, dout, scr;
+  DevBuf<rgfb::Coef3> c3;
+  DevBuf<double2> c1;
+  sig.upload(sigma, m);
+  din.upload(in, static_cast<size_t>(m * nlines));
+  dout.alloc(static_cast<size_t>(m * nlines));
+  scr.alloc(static_cast<size_t>(m * nlines));
+  if (order == 3)
+    c3.alloc(m);
+  else
+    c1.alloc(m);
+  rgfb::k_coefficients_1d<<<grid_for(m, 128), 128>>>(sig.p, m, order, k, calibration, c3.p,
+                                                    c1.p);
+  CUDA_OK(cudaGetLastError());
+  rgfb::k_apply_1d<<<grid_for(nlines, 64, 1 << 20), 64>>>(din.p, dout.p, c3.p, c1.p, m, nlines,
+                                                          order, k, transpose, scr.p);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemcpy(out, dout.p, static_cast<size_t>(m * nlines) * sizeof(double),
+                     cudaMemcpyDeviceToHost));
+}
+
+int rgf_rf3_apply_1d(const double* in, const double* sigma, int64_t m, int64_t nlines,
+                     int calibration, int transpose, double* out) {
+  return guarded([&] {
+    for (int64_t i = 0; i < m; ++i)
+      if (!(sigma[i] > 0)) throw InvalidArgument("rf3_filter_scalars: sigma must be positive");
+    if (m < 4) throw InvalidArgument("rf3 filter: segment length must be >= 4");
+    if (nlines < 1) throw InvalidArgument("rf3 filter: nlines must be >= 1");
+    apply_1d(in, sigma, m, nlines, 3, 1, calibration, transpose, out);
+  });
+}
+
+int rgf_rf1_apply_1d(const double* in, const double* sigma, int64_t m, int64_t nlines, int k,
+                     int transpose, double* out) {
+  return guarded([&] {
+    for (int64_t i = 0; i < m; ++i)
+      if (!(sigma[i] > 0)) throw InvalidArgument("rf1_coefficients: sigma must be positive");
+    if (k < 1) throw InvalidArgument("rf1_coefficients: k must be >= 1");
+    if (m < 2) throw InvalidArgument("rf1 filter: segment length must be >= 2");
+    if (nlines < 1) throw InvalidArgument("rf1 filter: nlines must be >= 1");
+    apply_1d(in, sigma, m, nlines, 1, k, RGF_CAL_YVV95, transpose, out);
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,255 @@
+"""GPU parity: the CUDA path through the C ABI against the CPU oracle on the
+same seeded inputs. Tolerances (north_star): relative max-norm 1e-12 for
+fp64, 1e-5 for fp32 (oracle = fp64 applied to the fp32-rounded input);
+segment/mask indexing bit-exact."""
+import numpy as np
+import pytest
+
+import oracle as O
+from helpers import checkered_mask, relmax, segments_numpy, uniform_grid
+
+pytestmark = pytest.mark.gpu
+
+TOL64 = 1e-12
+TOL32 = 1e-5
+
+
+@pytest.fixture(scope="module")
+def P():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    import paper_1404_5756_b200 as P
+    return P
+
+
+def build_pair(P, g, rx, ry, order=3, k=1, unit_dc=True, ghost=None, variance=None,
+               calibration=0, grid_ghost=0):
+    grid = P.Grid2D(g["nx"], g["ny"], g["dx"], g["dy"], g["mask"], grid_ghost)
+    opts = P.CovarianceOptions(order=P.FilterOrder(order), k_iterations=k, unit_dc=unit_dc,
+                               ghost_width=ghost, variance=variance,
+                               calibration=P.Rf3Calibration(calibration))
+    gpu = P.HorizontalCovarianceOp(grid, P.ScaleField(rx, ry), opts)
+    cpu = O.OracleOp(g["nx"], g["ny"], g["dx"], g["dy"], g["mask"], rx, ry, order=order,
+                     k_iterations=k, unit_dc=unit_dc, ghost_width=ghost, variance=variance,
+                     threads=4, calibration=calibration, grid_ghost_width=grid_ghost)
+    return gpu, cpu
+
+
+def random_case(seed, nx=57, ny=43, nlev=3, sea=0.8, smin=1.2, smax=4.5):
+    rng = np.random.default_rng(seed)
+    g = uniform_grid(nx, ny, 5000.0, 7000.0, nlev=nlev)
+    g["dx"] = 5000.0 * rng.uniform(0.7, 1.3, (ny, nx))
+    g["mask"] = checkered_mask(nx, ny, seed + 1, sea, nlev=nlev)
+    rx = g["dx"] * rng.uniform(smin, smax, (ny, nx))
+    ry = g["dy"] * rng.uniform(smin, smax, (ny, nx))
+    return g, rx, ry
+
+
+KINDS = ["GX", "GY", "GXT", "GYT", "V", "VT", "B", "GYGX"]
+
+
+@pytest.mark.parametrize("order,k", [(3, 1), (1, 1), (1, 5)])
+def test_all_kinds_fp64_random_masks(P, order, k):
+    g, rx, ry = random_case(10 + order + k)
+    var = np.random.default_rng(2).uniform(0.5, 2.0, (3, 43, 57))
+    gpu, cpu = build_pair(P, g, rx, ry, order=order, k=k, variance=var)
+    f = np.random.default_rng(3).standard_normal((2, 3, 43, 57))
+    for name in KINDS:
+        kind = getattr(P, name)
+        got = gpu.apply(kind, f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
+        land = ~g["mask"]
+        assert np.all(got[:, land] == 0.0), name
+
+
+@pytest.mark.parametrize("order,k", [(3, 1), (1, 5)])
+def test_fp32_storage(P, order, k):
+    g, rx, ry = random_case(40 + order)
+    gpu, cpu = build_pair(P, g, rx, ry, order=order, k=k)
+    f32 = np.random.default_rng(4).standard_normal((1, 3, 43, 57)).astype(np.float32)
+    for name in ("GYGX", "VT", "B"):
+        got = gpu.apply(getattr(P, name), f32)
+        assert got.dtype == np.float32
+        want = cpu.apply(getattr(O, name), f32.astype(np.float64))
+        assert relmax(got, want) <= TOL32, (name, relmax(got, want))
+
+
+def test_segments_bit_exact(P):
+    g, rx, ry = random_case(5, nx=64, ny=50, nlev=4, sea=0.6)
+    gpu, _ = build_pair(P, g, rx, ry)
+    for d in (0, 1):
+        off, segs = gpu.segments(d)
+        roff, rsegs = segments_numpy(g["mask"], d)
+        assert np.array_equal(off, roff)
+        assert np.array_equal(segs, rsegs)
+
+
+def test_coefficient_tables(P):
+    g, rx, ry = random_case(6, sea=0.7)
+    for order, k in ((3, 1), (1, 5)):
+        gpu, _ = build_pair(P, g, rx, ry, order=order, k=k)
+        any_sea = g["mask"].any(axis=0)
+        for d, (r, s) in enumerate(((rx, g["dx"]), (ry, g["dy"]))):
+            c = gpu.coefficients(d)
+            sig = np.where(any_sea, r / s, 1.0)
+            for idx in zip(*np.nonzero(any_sea)):
+                if order == 3:
+                    want = O.rf3_filter_scalars(sig[idx])
+                    assert c["alpha1"][idx] == want[0]
+                    assert c["alpha2"][idx] == want[1]
+                    assert c["alpha3"][idx] == want[2]
+                    assert abs(c["beta"][idx] - want[3]) <= 4 * np.spacing(abs(want[3]))
+                    assert c["inv_dc"][idx] == 1.0 / (np.sqrt(2 * np.pi) * sig[idx])
+                else:
+                    want = O.rf1_coefficients(sig[idx], k)
+                    assert c["alpha1"][idx] == want[0]
+                    assert c["beta"][idx] == want[1]
+
+
+def test_scalar_builders(P, golden):
+    for row in golden["kGolden"]["rows"]:
+        t = P.rf3_coefficients(row["sigma"])
+        o = O.rf3_coefficients(row["sigma"])
+        assert (t.a0, t.a1, t.a2, t.a3, t.alpha1, t.alpha2, t.alpha3) == tuple(o[:7])
+        assert abs(t.beta - o[7]) <= 4 * np.spacing(abs(o[7]))
+        assert abs(t.beta - row["beta"]) <= 1e-12 * abs(row["beta"])
+    for cal in (0, 1, 2):
+        for s in (0.05, 0.7, 2.5, 7.3, 14.0):
+            f = P.rf3_filter_scalars(s, P.Rf3Calibration(cal))
+            o = O.rf3_filter_scalars(s, cal)
+            assert (f.alpha1, f.alpha2, f.alpha3, f.q) == (o[0], o[1], o[2], o[4])
+            assert abs(f.beta - o[3]) <= 4 * np.spacing(abs(o[3]))
+    for s in (0.5, 2.0, 25.0):
+        for k in (1, 5, 10):
+            a = P.rf1_coefficients(s, k)
+            o = O.rf1_coefficients(s, k)
+            assert (a.alpha, a.beta) == (o[0], o[1])
+    with pytest.raises(P.InvalidArgument, match="sigma must be positive"):
+        P.rf3_coefficients(0.0)
+
+
+def test_1d_entry_points(P):
+    rng = np.random.default_rng(9)
+    m = 75
+    sig = rng.uniform(1.0, 5.0, m)
+    x = rng.standard_normal((6, m))
+    for tr in (False, True):
+        got = (P.rf3_apply_transpose_1d if tr else P.rf3_apply_1d)(x, sig)
+        for i in range(6):
+            want = O.rf3_apply_1d(x[i], sig, transpose=tr)
+            assert relmax(got[i], want) <= 1e-13
+        got = (P.rf1_apply_transpose_1d if tr else P.rf1_apply_1d)(x, sig, 3)
+        for i in range(6):
+            want = O.rf1_apply_1d(x[i], sig, 3, transpose=tr)
+            assert relmax(got[i], want) <= 1e-13
+    with pytest.raises(P.InvalidArgument, match="segment length must be >= 4"):
+        P.rf3_apply_1d(np.zeros(3), 2.0)
+
+
+def test_c1_config_parity_and_gaussian(P):
+    from paper_1404_5756_b200 import synth
+    c = synth.make_config("C1")
+    f = synth.make_field(c)
+    g = dict(nx=c.nx, ny=c.ny, dx=c.dx, dy=c.dy, mask=c.mask)
+    for order, k in ((3, 1), (1, 5)):
+        gpu, cpu = build_pair(P, g, c.rx, c.ry, order=order, k=k)
+        got = gpu.apply(P.GYGX, f)
+        want = cpu.apply(O.GYGX, f)
+        assert relmax(got, want) <= TOL64
+    # impulse-only run against the analytic Gaussian (unit_dc=false,
+    # unit-sum error as diagnostics.cpp:86-93)
+    gpu, _ = build_pair(P, g, c.rx, c.ry, unit_dc=False)
+    d = np.zeros((c.ny, c.nx))
+    d[c.ny // 2, c.nx // 2] = 1.0
+    h = gpu.apply(P.GYGX, d)
+    gx = synth.analytic_gaussian(c.nx, c.nx // 2, 4.0)
+    gy = synth.analytic_gaussian(c.ny, c.ny // 2, 4.0)
+    err = np.linalg.norm(h / h.sum() - np.outer(gy, gx))
+    assert err < 0.02
+
+
+def test_edge_cases(P):
+    rng = np.random.default_rng(21)
+    # tiny grid, ghost_width=0 with short segments passing through
+    g = uniform_grid(5, 4)
+    g["mask"][:, :, 2] = False
+    rx = ry = np.full((4, 5), 12000.0)
+    gpu, cpu = build_pair(P, g, rx, ry, unit_dc=False, ghost=0)
+    f = rng.standard_normal((4, 5))
+    for kind in ("GX", "GY", "B"):
+        assert np.array_equal(gpu.apply(getattr(P, kind), f), cpu.apply(getattr(O, kind), f))
+    # all-land level, single-point segments, per-level ghost widths
+    nx, ny = 31, 17
+    g = uniform_grid(nx, ny, nlev=4)
+    g["mask"][0] = False
+    g["mask"][1] = checkered_mask(nx, ny, 2, 0.3)[0]
+    g["mask"][2] = checkered_mask(nx, ny, 3, 0.9)[0]
+    rx = 6000.0 * rng.uniform(1.0, 6.0, (ny, nx))
+    ry = 6000.0 * rng.uniform(1.0, 6.0, (ny, nx))
+    gpu, cpu = build_pair(P, g, rx, ry)
+    for lev in range(4):
+        assert gpu.effective_ghost_width(lev) == cpu.ghost_width(lev)
+    f = rng.standard_normal((4, ny, nx))
+    for kind in ("V", "VT", "B"):
+        got, want = gpu.apply(getattr(P, kind), f), cpu.apply(getattr(O, kind), f)
+        assert relmax(got, want) <= TOL64
+        assert np.all(got[0] == 0.0)
+    # ghost resolution (test_covariance.cpp:348-359)
+    g = uniform_grid(16, 16)
+    r = np.full((16, 16), 12000.0)
+    assert build_pair(P, g, r, r)[0].effective_ghost_width() == 18
+    assert build_pair(P, g, r, r, grid_ghost=7)[0].effective_ghost_width() == 7
+    assert build_pair(P, g, r, r, grid_ghost=7, ghost=0)[0].effective_ghost_width() == 0
+
+
+def test_reference_error_messages(P):
+    g = uniform_grid(8, 8)
+    r = np.full((8, 8), 12000.0)
+    with pytest.raises(P.InvalidArgument, match="single-iteration by construction"):
+        build_pair(P, g, r, r, order=3, k=2)
+    with pytest.raises(P.InvalidArgument, match="k_iterations must be >= 1"):
+        build_pair(P, g, r, r, order=1, k=0)
+    bad = r.copy()
+    bad[3, 5] = -1.0
+    with pytest.raises(P.InvalidArgument, match=r"non-positive or non-finite radius at sea point \(5,3\)"):
+        build_pair(P, g, bad, r)
+    g2 = uniform_grid(8, 8)
+    g2["dx"][1, 1] = 0.0
+    with pytest.raises(P.InvalidArgument, match="grid spacing must be strictly positive"):
+        build_pair(P, g2, r, r)
+
+
+def test_deterministic_reruns(P):
+    g, rx, ry = random_case(77)
+    gpu, _ = build_pair(P, g, rx, ry)
+    f = np.random.default_rng(1).standard_normal((3, 43, 57))
+    a = gpu.apply(P.B, f)
+    b = gpu.apply(P.B, f)
+    assert np.array_equal(a, b)
+
+
+def test_c2_subset_forward_adjoint(P):
+    from paper_1404_5756_b200 import synth
+    c = synth.make_config("C2", nlev=6)
+    g = dict(nx=c.nx, ny=c.ny, dx=c.dx, dy=c.dy, mask=c.mask)
+    f = synth.make_field(c)
+    for order, k in ((3, 1), (1, 5)):
+        gpu, cpu = build_pair(P, g, c.rx, c.ry, order=order, k=k)
+        for kind in ("GYGX", "VT"):
+            got = gpu.apply(getattr(P, kind), f)
+            want = cpu.apply(getattr(O, kind), f)
+            assert relmax(got, want) <= TOL64, (order, kind, relmax(got, want))
+
+
+def test_torch_device_path(P):
+    import torch
+    g, rx, ry = random_case(88)
+    gpu, cpu = build_pair(P, g, rx, ry)
+    f = np.random.default_rng(5).standard_normal((2, 3, 43, 57))
+    t = torch.from_numpy(f).cuda()
+    out = gpu.apply(P.GYGX, t)
+    torch.cuda.synchronize()
+    assert relmax(out.cpu().numpy(), cpu.apply(O.GYGX, f)) <= TOL64
+    assert gpu.launch_count() > 0
