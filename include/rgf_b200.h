@@ -103,7 +103,7 @@ int rgf_op_destroy(rgf_op* op);
 /* apply_gx / apply_gy / apply_gx_transpose / apply_gy_transpose / apply_v /
  * apply_v_transpose / apply_b (covariance.cpp:362-398), out of place.
  * in/out hold nvar*nlev*ny*nx elements of `dtype`. memory = RGF_HOST or
- * RGF_DEVICE. stream: a cudaStream_t or NULL (per-thread default stream).
+ * RGF_DEVICE. stream: a cudaStream_t or NULL (the legacy default stream).
  * Device applies are asynchronous on `stream`; host applies return after the
  * result is in `out`. */
 int rgf_op_apply(rgf_op* op, int kind, int dtype, const void* in, void* out, int64_t nvar,

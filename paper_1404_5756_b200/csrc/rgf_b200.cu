@@ -9,6 +9,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <stdexcept>
@@ -120,6 +121,13 @@ struct rgf_op {
   int64_t scratch_threads = 0, scratch_slab = 0;
   cudaStream_t own_stream = nullptr;
   unsigned long long launches = 0;
+  // streaming 3rd-RF path: bit-packed masks, closure classes and tables
+  bool stream_ok = false;
+  DevBuf<uint64_t> bits[2];
+  int64_t words[2] = {0, 0};
+  DevBuf<int> cls_d;
+  DevBuf<double> clos;  // [class][dir][nh][18]
+  int nclass = 0;
   std::mutex mu;  // apply() is const in the reference; serialize buffer reuse
 
   ~rgf_op() {
@@ -139,7 +147,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
   const DirData& d = dir == 0 ? op->dx_ : op->dy_;
   const int64_t lines = nvar * op->nlev * (dir == 0 ? op->ny : op->nx);
 
-  if (op->order == 3 && rgfb::stream_supported(op->nx, op->ny)) {
+  if (op->stream_ok) {
     rgfb::StreamArgs a{};
     a.dir = dir;
     a.transpose = transpose;
@@ -149,10 +157,12 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.nlev = op->nlev;
     a.nvar = nvar;
     a.c3 = d.c3.p;
-    a.idc = d.idc.p;
-    a.seg_off = d.seg_off.p;
-    a.segs = d.segs.p;
+    a.idc = op->unit_dc ? d.idc.p : nullptr;
+    a.bits = op->bits[dir].p;
+    a.words = op->words[dir];
     a.ghost = op->ghost_d.p;
+    a.cls = op->cls_d.p;
+    a.clos = op->clos.p;
     a.pre_scale = pre;
     a.post_scale = post;
     op->launches += rgfb::launch_stream_sweep<T>(in, out, a, st);
@@ -415,6 +425,55 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
       CUDA_OK(cudaGetLastError());
       build_segments(op.get(), mask.p, dir, d);
     }
+    // Streaming 3rd-RF path (sweep_stream.cuh). Needs every level's ghost
+    // width >= 3 (then no segment can fall under the pass-through length,
+    // covariance.cpp:260-269) and is skipped when RGF_B200_EXACT=1 selects
+    // the bit-exact segment-serial kernel.
+    {
+      const char* ex = std::getenv("RGF_B200_EXACT");
+      const bool exact = ex && ex[0] == '1';
+      const int64_t gmin = *std::min_element(op->ghost.begin(), op->ghost.end());
+      if (op->order == 3 && !exact && gmin >= 3) {
+        std::vector<int64_t> classes;
+        std::vector<int> cls(g->nlev);
+        for (int64_t l = 0; l < g->nlev; ++l) {
+          auto it = std::find(classes.begin(), classes.end(), op->ghost[l]);
+          if (it == classes.end()) {
+            classes.push_back(op->ghost[l]);
+            it = classes.end() - 1;
+          }
+          cls[l] = static_cast<int>(it - classes.begin());
+        }
+        op->nclass = static_cast<int>(classes.size());
+        op->cls_d.upload(cls.data(), cls.size());
+        op->clos.alloc(static_cast<size_t>(op->nclass) * 2 * nh * 18);
+        const int threads = 128;
+        const int blocks = grid_for(nh, threads, 148 * 8);
+        const int64_t slab = op->gmax + 1;
+        DevBuf<double> scr;
+        scr.alloc(static_cast<size_t>(blocks) * threads * slab);
+        for (int c = 0; c < op->nclass; ++c)
+          for (int dir = 0; dir < 2; ++dir) {
+            const DirData& d = dir == 0 ? op->dx_ : op->dy_;
+            rgfb::k_closures<<<blocks, threads>>>(d.c3.p, nh, static_cast<int>(classes[c]),
+                                                  op->clos.p + (static_cast<int64_t>(c) * 2 + dir) * nh * 18,
+                                                  scr.p, slab);
+            CUDA_OK(cudaGetLastError());
+          }
+        for (int dir = 0; dir < 2; ++dir) {
+          const int64_t n = dir == 0 ? g->nx : g->ny;
+          const int64_t nl = dir == 0 ? g->ny : g->nx;
+          op->words[dir] = (n + 63) / 64;
+          const int64_t tot = g->nlev * nl * op->words[dir];
+          op->bits[dir].alloc(tot);
+          rgfb::k_pack_bits<<<grid_for(tot, 256), 256>>>(mask.p, dir, g->nx, g->ny, g->nlev,
+                                                         op->words[dir], op->bits[dir].p);
+          CUDA_OK(cudaGetLastError());
+        }
+        CUDA_OK(cudaDeviceSynchronize());
+        op->stream_ok = true;
+      }
+    }
     if (opt->variance) {
       op->variance.upload(opt->variance, static_cast<size_t>(nh * g->nlev));
       op->has_variance = true;
@@ -445,7 +504,8 @@ int rgf_op_apply(rgf_op* op, int kind, int dtype, const void* in, void* out, int
     CUDA_OK(cudaSetDevice(op->device));
     const size_t esz = dtype == RGF_F64 ? 8 : 4;
     const size_t count = static_cast<size_t>(nvar * op->nlev * op->nx * op->ny);
-    cudaStream_t st = stream ? static_cast<cudaStream_t>(stream) : op->own_stream;
+    // NULL = the legacy default stream (torch's default stream hands us 0)
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
     const void* din = in;
     void* dout = out;
     if (memory == RGF_HOST) {
@@ -490,6 +550,7 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
   return guarded([&] {
     if (!op || !out) throw InvalidArgument("device_bytes: null argument");
     uint64_t b = op->ghost_d.bytes() + op->variance.bytes() + op->in_d.bytes() +
+                 op->bits[0].bytes() + op->bits[1].bytes() + op->clos.bytes() + op->cls_d.bytes() +
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})
       b += d->c3.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes();

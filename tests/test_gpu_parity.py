@@ -253,3 +253,32 @@ def test_torch_device_path(P):
     torch.cuda.synchronize()
     assert relmax(out.cpu().numpy(), cpu.apply(O.GYGX, f)) <= TOL64
     assert gpu.launch_count() > 0
+
+
+def test_exact_mode_matches_oracle_to_rounding(P, monkeypatch):
+    """RGF_B200_EXACT=1 selects the segment-serial kernel with the reference's
+    unfused arithmetic; only beta's pow() may differ by an ulp."""
+    g, rx, ry = random_case(123)
+    monkeypatch.setenv("RGF_B200_EXACT", "1")
+    gpu, cpu = build_pair(P, g, rx, ry)
+    monkeypatch.delenv("RGF_B200_EXACT")
+    f = np.random.default_rng(8).standard_normal((3, 43, 57))
+    for name in ("GYGX", "VT"):
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= 1e-14, (name, relmax(got, want))
+
+
+def test_streaming_vs_exact_path(P, monkeypatch):
+    """The streaming path (FMA + right-ghost closure) against the exact
+    segment-serial path on a C5-like mask with sigma up to 10 (G = 90)."""
+    from paper_1404_5756_b200 import synth
+    c = synth.make_config("C5", nlev=2, nx=600, ny=300)
+    g = dict(nx=c.nx, ny=c.ny, dx=c.dx, dy=c.dy, mask=c.mask)
+    f = synth.make_field(c)
+    fast, cpu = build_pair(P, g, c.rx, c.ry)
+    assert fast.effective_ghost_width() == cpu.ghost_width()
+    for name in ("GYGX", "VT", "B"):
+        got = fast.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
