@@ -1,36 +1,37 @@
 // Streaming 3rd-RF sweeps (forward G_dir and adjoint G_dir^T).
 //
-// One thread per (plane, line); adjacent threads own adjacent lines, so a
-// y-sweep (lines = columns) reads and writes every row as one coalesced
-// 256 B warp access, and an x-sweep reads 32 B sectors per lane. Each line
-// is processed as the reference does segment by segment
-// (covariance.cpp:228-352), fused into two streaming passes:
+// Each chain is one (plane, line) of the field; the reference processes it
+// segment by segment (covariance.cpp:228-352). Here every chain runs two
+// streaming passes over the whole line:
 //
 //   A (ascending k): zero-state causal recursion inside every sea segment
-//     (rf3.hpp:217-239; the reference's startup rows are exactly a zero
-//     initial state), intermediate stored to `out`; land stores 0.
+//     (rf3.hpp:217-239 — the reference's startup rows are exactly a zero
+//     initial state); the intermediate is stored to `out`, land stores 0.
 //   D (descending k): at each segment end j the anti-causal recursion is
-//     entered through the right-ghost closure (below), then runs down the
-//     segment (rf3.hpp:241-262), scales by inv_dc (covariance.cpp:317) and
-//     the optional variance, and overwrites `out`. Land stays exactly 0.
+//     entered through the right-ghost closure (closures.cuh), runs down the
+//     segment (rf3.hpp:241-262), is scaled by inv_dc (covariance.cpp:317)
+//     and the optional variance, and overwrites `out`. Land stays exactly 0.
 //
-// The adjoint (rf3.hpp:264-286, applied as backward_transpose then
-// forward_transpose, covariance.cpp:325-333) is run in the equivalent
-// register-resident gather form with the reference's accumulation order
-// (alpha3 term, then alpha2, then alpha1).
+// The adjoint (rf3.hpp:264-286, backward_transpose then forward_transpose,
+// covariance.cpp:325-333) runs in the equivalent register-resident gather
+// form with the reference's accumulation order (alpha3 term, then alpha2,
+// then alpha1).
 //
-// Right-ghost closure: the G imaginary points beyond a segment end carry zero
-// input and the end point's replicated coefficients (covariance.cpp:38-44),
-// so "continue the causal pass G steps, restart the anti-causal pass at the
-// far end, come back G steps" is a fixed linear map from the 3-value causal
-// state at j to the 3-value anti-causal state entering j. It depends only on
-// (coefficients at j, G) and is precomputed per point and per distinct ghost
-// width at construction (k_closures). Left ghosts provably never affect a
-// 3rd-RF segment (zero input, zero state), so they cost
-// nothing. The recursion uses FMA with the alpha1 term last, so one DFMA
-// sits on the loop-carried path (11 cycles/step measured vs 33 for the
-// reference's unfused order; profiles/r01_machine_probe.log).
+// Left ghosts never affect a 3rd-RF segment (zero input, zero state;
+// SURVEY.md §8a) and cost nothing. The recursion uses FMA with the alpha1
+// term last, so one DFMA sits on the loop-carried path (11 cycles/step vs
+// 33 for the reference's unfused order, profiles/r01_machine_probe.log).
+//
+// Thread mappings (memory-system driven):
+//   y-sweep (lines = columns): lanes own adjacent columns, so every row step
+//     is one coalesced warp access; each thread carries L planes of its
+//     column (ILP, and one coefficient load serves L chains).
+//   x-sweep (lines = rows): lanes own the same row of consecutive planes, so
+//     the coefficient loads are warp-uniform broadcasts; each lane streams
+//     its row in 8-element vector batches (64 B fp64 / 32 B fp32).
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace rgfb {
@@ -43,8 +44,8 @@ struct StreamArgs {
   const uint64_t* bits;     // bit-packed masks for this direction
   int64_t words;            // 64-bit words per line
   const int* ghost;         // per level
-  const int* cls;           // per level closure class (-1: no right ghosts)
-  const double* clos;       // [class][dir][nh][18]: M (9) then M^T-closure (9)
+  const int* cls;           // per level closure class
+  const double* clos;       // [class][dir][nh][18]: M (9) then adjoint closure (9)
   const double* pre_scale;  // optional (nlev*nh) input multiplier (variance)
   const double* post_scale; // optional (nlev*nh) output multiplier
 };
@@ -54,289 +55,434 @@ __device__ __forceinline__ int mbit(const uint64_t* w, int64_t k, int64_t n) {
   return static_cast<int>((__ldg(reinterpret_cast<const unsigned long long*>(w) + (k >> 6)) >>
                            (k & 63)) & 1ull);
 }
-
-template <typename T>
-__device__ __forceinline__ double ldv(const T* p) {
-  return static_cast<double>(*p);
+__device__ __forceinline__ uint64_t ldw(const uint64_t* w, int64_t i) {
+  return __ldg(reinterpret_cast<const unsigned long long*>(w) + i);
 }
-
 __device__ __forceinline__ Coef3 ldc(const Coef3* p) {
   const double2 lo = __ldg(reinterpret_cast<const double2*>(p));
   const double2 hi = __ldg(reinterpret_cast<const double2*>(p) + 1);
   return Coef3{lo.x, lo.y, hi.x, hi.y};
 }
+template <typename T>
+__device__ __forceinline__ double ldv(const T* p) {  // coherent: reads this thread's writes
+  return static_cast<double>(*p);
+}
 
-template <typename T, int DIR, bool TR>
-__global__ void __launch_bounds__(128) k_stream(const T* __restrict__ in, T* __restrict__ out,
-                                                StreamArgs a) {
-  const int64_t n = DIR == 0 ? a.nx : a.ny;
-  const int64_t nlines = DIR == 0 ? a.ny : a.nx;
-  const int64_t nh = a.nx * a.ny;
-  const int64_t stride = DIR == 0 ? 1 : a.nx;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+// ---------------------------------------------------------- chain states
+struct FwdA {  // causal: p_{k-1}, p_{k-2}, p_{k-3}
+  double p1 = 0.0, p2 = 0.0, p3 = 0.0;
+  __device__ __forceinline__ double step(const Coef3& c, double s, bool sea) {
+    const double t = fma(c.a1, p1, fma(c.a2, p2, fma(c.a3, p3, c.b * s)));
+    p3 = sea ? p2 : 0.0;
+    p2 = sea ? p1 : 0.0;
+    p1 = sea ? t : 0.0;
+    return p1;
+  }
+};
+struct FwdD {  // anti-causal: q_{k+1}, q_{k+2}, q_{k+3}
+  double q1 = 0.0, q2 = 0.0, q3 = 0.0;
+  __device__ __forceinline__ void enter(const double* M, double x0, double x1, double x2) {
+    q1 = fma(M[0], x0, fma(M[1], x1, M[2] * x2));
+    q2 = fma(M[3], x0, fma(M[4], x1, M[5] * x2));
+    q3 = fma(M[6], x0, fma(M[7], x1, M[8] * x2));
+  }
+  __device__ __forceinline__ double step(const Coef3& c, double z) {
+    const double q = fma(c.a1, q1, fma(c.a2, q2, fma(c.a3, q3, c.b * z)));
+    q3 = q2;
+    q2 = q1;
+    q1 = q;
+    return q;
+  }
+};
+struct AdjA {  // transpose of the anti-causal pass, gather form
+  double u1 = 0.0, x1 = 0.0, y21 = 0.0, y22 = 0.0, y31 = 0.0, y32 = 0.0, y33 = 0.0;
+  __device__ __forceinline__ double step(const Coef3& c, double w, bool sea) {
+    double u = fma(x1, u1, (w + y33) + y22);
+    if (!sea) {
+      u = 0.0;
+      y31 = y32 = 0.0;
+      y21 = 0.0;
+    }
+    y33 = y32;
+    y32 = y31;
+    y31 = c.a3 * u;
+    y22 = y21;
+    y21 = c.a2 * u;
+    x1 = c.a1;
+    u1 = u;
+    return u;
+  }
+};
+struct AdjD {  // transpose of the causal pass, gather form
+  double U1 = 0.0, X1 = 0.0, Y21 = 0.0, Y22 = 0.0, Y31 = 0.0, Y32 = 0.0, Y33 = 0.0;
+  __device__ __forceinline__ void reset() { U1 = X1 = Y21 = Y22 = Y31 = Y32 = Y33 = 0.0; }
+  // P1..P3: pending causal-transpose contributions of u_j, u_{j-1}, u_{j-2}
+  // into the first three ghosts; the closure returns u'_{j+1..j+3}.
+  __device__ __forceinline__ void enter(const double* M, const Coef3& c, const Coef3& cm1,
+                                        const Coef3& cm2, double uj, double ujm1, double ujm2) {
+    const double P1 = fma(c.a1, uj, fma(cm1.a2, ujm1, cm2.a3 * ujm2));
+    const double P2 = fma(c.a2, uj, cm1.a3 * ujm1);
+    const double P3 = c.a3 * uj;
+    const double g1 = fma(M[0], P1, fma(M[1], P2, M[2] * P3));
+    const double g2 = fma(M[3], P1, fma(M[4], P2, M[5] * P3));
+    const double g3 = fma(M[6], P1, fma(M[7], P2, M[8] * P3));
+    U1 = g1;
+    X1 = c.a1;
+    Y21 = c.a2 * g1;
+    Y22 = c.a2 * g2;
+    Y31 = c.a3 * g1;
+    Y32 = c.a3 * g2;
+    Y33 = c.a3 * g3;
+  }
+  __device__ __forceinline__ double step(const Coef3& c, double z) {
+    const double v = c.b * z;
+    const double u = fma(X1, U1, (v + Y33) + Y22);
+    Y33 = Y32;
+    Y32 = Y31;
+    Y31 = c.a3 * u;
+    Y22 = Y21;
+    Y21 = c.a2 * u;
+    X1 = c.a1;
+    U1 = u;
+    return c.b * u;
+  }
+};
+
+// Segment-end entry of pass D for chain data (dst: this chain's line, W: its
+// mask words, CL: its closure row, C: coefficient line, stride along k).
+template <bool TR, typename T, typename DState>
+__device__ __forceinline__ void enter_segment(DState& st, int64_t k, int64_t n, int G,
+                                              const T* dst, const uint64_t* W, const double* CL,
+                                              const Coef3* C, int64_t stride, const Coef3& c,
+                                              double z0) {
+  if constexpr (TR) st.reset();
+  else st.q1 = st.q2 = st.q3 = 0.0;
+  if (k < n - 1 && G > 0) {
+    const int s1 = mbit(W, k - 1, n);
+    const int s2 = s1 ? mbit(W, k - 2, n) : 0;
+    const double z1 = s1 ? ldv(dst + (k - 1) * stride) : 0.0;
+    const double z2 = s2 ? ldv(dst + (k - 2) * stride) : 0.0;
+    const double* M = CL + k * stride * 18;
+    if constexpr (!TR) {
+      st.enter(M, z0, z1, z2);
+    } else {
+      const Coef3 cm1 = s1 ? ldc(C + (k - 1) * stride) : Coef3{0, 0, 0, 0};
+      const Coef3 cm2 = s2 ? ldc(C + (k - 2) * stride) : Coef3{0, 0, 0, 0};
+      st.enter(M + 9, c, cm1, cm2, z0, z1, z2);
+    }
+  }
+}
+
+// ================================================================ y-sweep
+template <typename T, bool TR, int L, int U>
+__global__ void __launch_bounds__(128) k_sweep_y(const T* __restrict__ in, T* __restrict__ out,
+                                                 StreamArgs a) {
+  const int64_t nx = a.nx, n = a.ny, nh = nx * n;
   const int64_t planes = a.nvar * a.nlev;
-  if (tid >= planes * nlines) return;
-  const int64_t plane = tid / nlines;
-  const int64_t line = tid - plane * nlines;
-  const int64_t lev = plane % a.nlev;
-  const int64_t hb = DIR == 0 ? line * a.nx : line;  // horizontal index of k=0
-  const T* src = in + plane * nh + hb;
-  T* dst = out + plane * nh + hb;
+  const int64_t groups = (planes + L - 1) / L;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= groups * nx) return;
+  const int64_t g = tid / nx, ix = tid - g * nx;
+  const Coef3* C = a.c3 + ix;
+  const double* IDC = a.idc ? a.idc + ix : nullptr;
+
+  const T* src[L];
+  T* dst[L];
+  const uint64_t* W[L];
+  const double* CL[L];
+  const double* PRE[L];
+  const double* POST[L];
+  int G[L];
+  bool on[L];
+#pragma unroll
+  for (int l = 0; l < L; ++l) {
+    const int64_t p = g * L + l;
+    on[l] = p < planes;
+    const int64_t pp = on[l] ? p : planes - 1;
+    const int64_t lev = pp % a.nlev;
+    src[l] = in + pp * nh + ix;
+    dst[l] = out + pp * nh + ix;
+    W[l] = a.bits + (lev * nx + ix) * a.words;
+    G[l] = a.ghost[lev];
+    const int cl = a.cls[lev];
+    CL[l] = a.clos + ((int64_t)(cl * 2 + 1) * nh + ix) * 18;
+    PRE[l] = a.pre_scale ? a.pre_scale + lev * nh + ix : nullptr;
+    POST[l] = a.post_scale ? a.post_scale + lev * nh + ix : nullptr;
+  }
+
+  // ------------------------------ pass A
+  {
+    typename std::conditional<TR, AdjA, FwdA>::type st[L];
+    uint64_t wc[L];
+    for (int64_t k0 = 0; k0 < n; k0 += U) {
+      if ((k0 & 63) == 0) {
+#pragma unroll
+        for (int l = 0; l < L; ++l) wc[l] = ldw(W[l], k0 >> 6);
+      }
+      Coef3 c[U];
+      double s[L][U];
+      double id[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + u;
+        if (k < n) {
+          c[u] = ldc(C + k * nx);
+          if (TR) id[u] = IDC ? __ldg(IDC + k * nx) : 1.0;
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            s[l][u] = on[l] ? ldv(src[l] + k * nx) : 0.0;
+            if (TR && PRE[l]) s[l][u] *= __ldg(PRE[l] + k * nx);
+          }
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + u;
+        if (k < n) {
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const bool sea = (wc[l] >> (k & 63)) & 1ull;
+            const double w = TR ? s[l][u] * id[u] : s[l][u];
+            const double r = st[l].step(c[u], w, sea);
+            if (on[l]) dst[l][k * nx] = static_cast<T>(r);
+          }
+        }
+      }
+    }
+  }
+  // ------------------------------ pass D
+  {
+    typename std::conditional<TR, AdjD, FwdD>::type st[L];
+    uint64_t wc[L];
+    int nxt[L];
+#pragma unroll
+    for (int l = 0; l < L; ++l) nxt[l] = 0;
+    int64_t widx = -1;
+    for (int64_t k0 = n - 1; k0 >= 0; k0 -= U) {
+      Coef3 c[U];
+      double z[L][U];
+      double id[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 - u;
+        if (k >= 0) {
+          c[u] = ldc(C + k * nx);
+          id[u] = (!TR && IDC) ? __ldg(IDC + k * nx) : 1.0;
+#pragma unroll
+          for (int l = 0; l < L; ++l) z[l][u] = on[l] ? ldv(dst[l] + k * nx) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 - u;
+        if (k >= 0) {
+          if ((k >> 6) != widx) {
+            widx = k >> 6;
+#pragma unroll
+            for (int l = 0; l < L; ++l) wc[l] = ldw(W[l], widx);
+          }
+#pragma unroll
+          for (int l = 0; l < L; ++l) {
+            const int sea = static_cast<int>((wc[l] >> (k & 63)) & 1ull);
+            if (sea && !nxt[l] && on[l])
+              enter_segment<TR>(st[l], k, n, G[l], dst[l], W[l], CL[l], C, nx, c[u], z[l][u]);
+            double o = st[l].step(c[u], z[l][u]);
+            if (!TR && IDC) o *= id[u];
+            if (POST[l]) o *= __ldg(POST[l] + k * nx);
+            if (on[l]) dst[l][k * nx] = static_cast<T>(sea ? o : 0.0);
+            nxt[l] = sea;
+          }
+        }
+      }
+    }
+  }
+}
+
+// ================================================================ x-sweep
+// Vector batch of 8 consecutive elements of one lane's row.
+template <typename T, bool VEC>
+__device__ __forceinline__ void ld8(const T* p, double (&v)[8], int cnt) {
+  if (VEC && cnt == 8) {
+    if constexpr (sizeof(T) == 8) {
+      const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const double2 t = q[i];
+        v[2 * i] = t.x;
+        v[2 * i + 1] = t.y;
+      }
+    } else {
+      const float4* q = reinterpret_cast<const float4*>(p);
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const float4 t = q[i];
+        v[4 * i] = t.x;
+        v[4 * i + 1] = t.y;
+        v[4 * i + 2] = t.z;
+        v[4 * i + 3] = t.w;
+      }
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < cnt ? static_cast<double>(p[i]) : 0.0;
+  }
+}
+template <typename T, bool VEC>
+__device__ __forceinline__ void st8(T* p, const double (&v)[8], int cnt) {
+  if (VEC && cnt == 8) {
+    if constexpr (sizeof(T) == 8) {
+      double2* q = reinterpret_cast<double2*>(p);
+#pragma unroll
+      for (int i = 0; i < 4; ++i) q[i] = make_double2(v[2 * i], v[2 * i + 1]);
+    } else {
+      float4* q = reinterpret_cast<float4*>(p);
+#pragma unroll
+      for (int i = 0; i < 2; ++i)
+        q[i] = make_float4(static_cast<float>(v[4 * i]), static_cast<float>(v[4 * i + 1]),
+                           static_cast<float>(v[4 * i + 2]), static_cast<float>(v[4 * i + 3]));
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      if (i < cnt) p[i] = static_cast<T>(v[i]);
+  }
+}
+__device__ __forceinline__ void ld8d(const double* p, double (&v)[8], int cnt, bool vec) {
+  if (vec && cnt == 8) {
+    const double2* q = reinterpret_cast<const double2*>(p);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const double2 t = __ldg(q + i);
+      v[2 * i] = t.x;
+      v[2 * i + 1] = t.y;
+    }
+  } else {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = i < cnt ? __ldg(p + i) : 0.0;
+  }
+}
+
+template <typename T, bool TR, bool VEC>
+__global__ void __launch_bounds__(128) k_sweep_x(const T* __restrict__ in, T* __restrict__ out,
+                                                 StreamArgs a) {
+  const int64_t n = a.nx, ny = a.ny, nh = n * ny;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= planes * ny) return;
+  const int64_t iy = tid / planes, p = tid - iy * planes;
+  const int64_t lev = p % a.nlev;
+  const int64_t hb = iy * n;
+  const T* src = in + p * nh + hb;
+  T* dst = out + p * nh + hb;
   const Coef3* C = a.c3 + hb;
   const double* IDC = a.idc ? a.idc + hb : nullptr;
   const double* PRE = a.pre_scale ? a.pre_scale + lev * nh + hb : nullptr;
   const double* POST = a.post_scale ? a.post_scale + lev * nh + hb : nullptr;
-  const uint64_t* W = a.bits + (lev * nlines + line) * a.words;
+  const uint64_t* W = a.bits + (lev * ny + iy) * a.words;
   const int G = a.ghost[lev];
-  const int cl = a.cls[lev];
-  const double* CL = cl >= 0 ? a.clos + ((int64_t)(cl * 2 + DIR) * nh + hb) * 18 : nullptr;
+  const double* CL = a.clos + ((int64_t)(a.cls[lev] * 2 + 0) * nh + hb) * 18;
+  const int64_t nb = (n + 7) / 8;
 
-  if (!TR) {
-    // ---------------- pass A: causal, zero state per segment
-    double p1 = 0.0, p2 = 0.0, p3 = 0.0;
-    uint64_t wcur = 0;
-    for (int64_t k = 0; k < n; ++k) {
-      if ((k & 63) == 0) wcur = __ldg(reinterpret_cast<const unsigned long long*>(W) + (k >> 6));
-      const bool sea = (wcur >> (k & 63)) & 1ull;
-      const Coef3 c = ldc(C + k * stride);
-      const double s = ldv(src + k * stride);
-      const double t = fma(c.a1, p1, fma(c.a2, p2, fma(c.a3, p3, c.b * s)));
-      p3 = sea ? p2 : 0.0;
-      p2 = sea ? p1 : 0.0;
-      p1 = sea ? t : 0.0;
-      dst[k * stride] = static_cast<T>(p1);
-    }
-    // ---------------- pass D: anti-causal, entered through the closure
-    double q1 = 0.0, q2 = 0.0, q3 = 0.0;
-    int sea_next = 0;  // sea(k+1)
-    wcur = 0;
-    double z0 = ldv(dst + (n - 1) * stride);
-    double zm1 = n >= 2 ? ldv(dst + (n - 2) * stride) : 0.0;
-    for (int64_t k = n - 1; k >= 0; --k) {
-      if (k == n - 1 || (k & 63) == 63)
-        wcur = __ldg(reinterpret_cast<const unsigned long long*>(W) + (k >> 6));
-      const int sea = static_cast<int>((wcur >> (k & 63)) & 1ull);
-      const double zm2 = k >= 2 ? ldv(dst + (k - 2) * stride) : 0.0;  // read-ahead
-      const Coef3 c = ldc(C + k * stride);
-      if (sea && !sea_next) {  // segment end j = k
-        q1 = q2 = q3 = 0.0;
-        if (k < n - 1 && G > 0) {
-          const int s1 = mbit(W, k - 1, n);
-          const int s2 = s1 ? mbit(W, k - 2, n) : 0;
-          const double x0 = z0, x1 = s1 ? zm1 : 0.0, x2 = s2 ? zm2 : 0.0;
-          const double* M = CL + k * stride * 18;
-          q1 = fma(M[0], x0, fma(M[1], x1, M[2] * x2));
-          q2 = fma(M[3], x0, fma(M[4], x1, M[5] * x2));
-          q3 = fma(M[6], x0, fma(M[7], x1, M[8] * x2));
+  // ------------------------------ pass A
+  {
+    typename std::conditional<TR, AdjA, FwdA>::type st;
+    uint64_t wc = 0;
+    for (int64_t b = 0; b < nb; ++b) {
+      const int64_t k0 = b * 8;
+      const int cnt = static_cast<int>(n - k0 < 8 ? n - k0 : 8);
+      if ((k0 & 63) == 0) wc = ldw(W, k0 >> 6);
+      double s[8], id[8], pr[8];
+      Coef3 c[8];
+      ld8<T, VEC>(src + k0, s, cnt);
+      if (TR) {
+        if (IDC) ld8d(IDC + k0, id, cnt, VEC);
+        if (PRE) ld8d(PRE + k0, pr, cnt, VEC);
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (u < cnt) c[u] = ldc(C + k0 + u);
+      double r[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        if (u < cnt) {
+          const bool sea = (wc >> ((k0 + u) & 63)) & 1ull;
+          double w = s[u];
+          if (TR) {
+            if (PRE) w *= pr[u];
+            if (IDC) w *= id[u];
+          }
+          r[u] = st.step(c[u], w, sea);
         }
       }
-      const double q = fma(c.a1, q1, fma(c.a2, q2, fma(c.a3, q3, c.b * z0)));
-      double o = q;
-      if (IDC) o *= __ldg(IDC + k * stride);
-      if (POST) o *= __ldg(POST + k * stride);
-      dst[k * stride] = static_cast<T>(sea ? o : 0.0);
-      q3 = q2;
-      q2 = q1;
-      q1 = q;
-      sea_next = sea;
-      z0 = zm1;
-      zm1 = zm2;
+      st8<T, VEC>(dst + k0, r, cnt);
     }
-  } else {
-    // ---------------- pass A: transpose of the anti-causal pass (gather form)
-    double u1 = 0.0, x1 = 0.0, y21 = 0.0, y22 = 0.0, y31 = 0.0, y32 = 0.0, y33 = 0.0;
-    uint64_t wcur = 0;
-    for (int64_t k = 0; k < n; ++k) {
-      if ((k & 63) == 0) wcur = __ldg(reinterpret_cast<const unsigned long long*>(W) + (k >> 6));
-      const bool sea = (wcur >> (k & 63)) & 1ull;
-      const Coef3 c = ldc(C + k * stride);
-      double w = ldv(src + k * stride);
-      if (PRE) w *= __ldg(PRE + k * stride);
-      if (IDC) w *= __ldg(IDC + k * stride);
-      double u = fma(x1, u1, (w + y33) + y22);
-      if (!sea) {
-        u = 0.0;
-        y31 = y32 = 0.0;
-        y21 = 0.0;
-      }
-      y33 = y32;
-      y32 = y31;
-      y31 = c.a3 * u;
-      y22 = y21;
-      y21 = c.a2 * u;
-      x1 = c.a1;
-      u1 = u;
-      dst[k * stride] = static_cast<T>(u);
-    }
-    // ---------------- pass D: transpose of the causal pass (gather form)
-    double U1 = 0.0, X1 = 0.0, Y21 = 0.0, Y22 = 0.0, Y31 = 0.0, Y32 = 0.0, Y33 = 0.0;
-    int sea_next = 0;
-    wcur = 0;
-    double z0 = ldv(dst + (n - 1) * stride);
-    double zm1 = n >= 2 ? ldv(dst + (n - 2) * stride) : 0.0;
-    for (int64_t k = n - 1; k >= 0; --k) {
-      if (k == n - 1 || (k & 63) == 63)
-        wcur = __ldg(reinterpret_cast<const unsigned long long*>(W) + (k >> 6));
-      const int sea = static_cast<int>((wcur >> (k & 63)) & 1ull);
-      const double zm2 = k >= 2 ? ldv(dst + (k - 2) * stride) : 0.0;
-      const Coef3 c = ldc(C + k * stride);
-      if (sea && !sea_next) {  // segment end j = k
-        U1 = X1 = Y21 = Y22 = Y31 = Y32 = Y33 = 0.0;
-        if (k < n - 1 && G > 0) {
-          const int s1 = mbit(W, k - 1, n);
-          const int s2 = s1 ? mbit(W, k - 2, n) : 0;
-          const double uj = z0, ujm1 = s1 ? zm1 : 0.0, ujm2 = s2 ? zm2 : 0.0;
-          const Coef3 cm1 = s1 ? ldc(C + (k - 1) * stride) : Coef3{0, 0, 0, 0};
-          const Coef3 cm2 = s2 ? ldc(C + (k - 2) * stride) : Coef3{0, 0, 0, 0};
-          // pending causal-transpose contributions into the ghosts
-          const double P1 = fma(c.a1, uj, fma(cm1.a2, ujm1, cm2.a3 * ujm2));
-          const double P2 = fma(c.a2, uj, cm1.a3 * ujm1);
-          const double P3 = c.a3 * uj;
-          const double* M = CL + k * stride * 18 + 9;
-          const double g1 = fma(M[0], P1, fma(M[1], P2, M[2] * P3));
-          const double g2 = fma(M[3], P1, fma(M[4], P2, M[5] * P3));
-          const double g3 = fma(M[6], P1, fma(M[7], P2, M[8] * P3));
-          U1 = g1;
-          X1 = c.a1;
-          Y21 = c.a2 * g1;
-          Y22 = c.a2 * g2;
-          Y31 = c.a3 * g1;
-          Y32 = c.a3 * g2;
-          Y33 = c.a3 * g3;
+  }
+  // ------------------------------ pass D
+  {
+    typename std::conditional<TR, AdjD, FwdD>::type st;
+    uint64_t wc = 0;
+    int nxt = 0;
+    for (int64_t b = nb - 1; b >= 0; --b) {
+      const int64_t k0 = b * 8;
+      const int cnt = static_cast<int>(n - k0 < 8 ? n - k0 : 8);
+      wc = ldw(W, k0 >> 6);
+      double z[8], id[8], po[8], r[8];
+      Coef3 c[8];
+      ld8<T, VEC>(dst + k0, z, cnt);
+      if (!TR && IDC) ld8d(IDC + k0, id, cnt, VEC);
+      if (POST) ld8d(POST + k0, po, cnt, VEC);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (u < cnt) c[u] = ldc(C + k0 + u);
+#pragma unroll
+      for (int u = 7; u >= 0; --u) {
+        if (u < cnt) {
+          const int64_t k = k0 + u;
+          const int sea = static_cast<int>((wc >> (k & 63)) & 1ull);
+          if (sea && !nxt) enter_segment<TR>(st, k, n, G, dst, W, CL, C, 1, c[u], z[u]);
+          double o = st.step(c[u], z[u]);
+          if (!TR && IDC) o *= id[u];
+          if (POST) o *= po[u];
+          r[u] = sea ? o : 0.0;
+          nxt = sea;
         }
       }
-      const double v = c.b * z0;
-      const double u = fma(X1, U1, (v + Y33) + Y22);
-      double o = c.b * u;
-      if (POST) o *= __ldg(POST + k * stride);
-      dst[k * stride] = static_cast<T>(sea ? o : 0.0);
-      Y33 = Y32;
-      Y32 = Y31;
-      Y31 = c.a3 * u;
-      Y22 = Y21;
-      Y21 = c.a2 * u;
-      X1 = c.a1;
-      U1 = u;
-      sea_next = sea;
-      z0 = zm1;
-      zm1 = zm2;
+      st8<T, VEC>(dst + k0, r, cnt);
     }
-  }
-}
-
-// ------------------------------------------------------------ closures
-// Per point p (horizontal), ghost width G, coefficients c = c3[p]:
-//  M (forward op): state (p_j, p_{j-1}, p_{j-2}) -> (q_{j+1}, q_{j+2}, q_{j+3})
-//    by G causal ghost steps with zero input, then the anti-causal pass from
-//    the far end with zero state (the reference's startup rows).
-//  Mt (adjoint): pending contributions (P1, P2, P3) into u_{j+1..j+3} ->
-//    (u'_{j+1}, u'_{j+2}, u'_{j+3}) by the causal-transpose gather over the
-//    ghosts, beta scaling, and the anti-causal-transpose gather back.
-// Ghost recursions use the reference's unfused left-to-right order.
-__global__ void k_closures(const Coef3* c3, int64_t nh, int G, double* out, double* scratch,
-                           int64_t slab) {
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  double* g = scratch + tid * slab;
-  for (int64_t p = tid; p < nh; p += (int64_t)gridDim.x * blockDim.x) {
-    const Coef3 c = c3[p];
-    double* o = out + p * 18;
-    for (int m = 0; m < 3; ++m) {
-      // forward closure, basis state e_m over (p_j, p_{j-1}, p_{j-2})
-      double pm1 = m == 0, pm2 = m == 1, pm3 = m == 2;
-      for (int k = 0; k < G; ++k) {
-        const double t = dadd(dadd(dmul(c.a1, pm1), dmul(c.a2, pm2)), dmul(c.a3, pm3));
-        pm3 = pm2;
-        pm2 = pm1;
-        pm1 = t;
-        g[k] = t;
-      }
-      double q1 = 0.0, q2 = 0.0, q3 = 0.0;
-      double r[3] = {0.0, 0.0, 0.0};
-      for (int k = G - 1; k >= 0; --k) {
-        const double t = dadd(dadd(dadd(dmul(c.b, g[k]), dmul(c.a1, q1)), dmul(c.a2, q2)),
-                              dmul(c.a3, q3));
-        q3 = q2;
-        q2 = q1;
-        q1 = t;
-        if (k < 3) r[k] = t;
-      }
-      o[0 + m] = r[0];
-      o[3 + m] = r[1];
-      o[6 + m] = r[2];
-
-      // adjoint closure, basis pending contributions e_m over (P1, P2, P3)
-      const double P1 = m == 0, P2 = m == 1, P3 = m == 2;
-      double u1 = 0.0, u2 = 0.0, u3 = 0.0;  // u_{k-1}, u_{k-2}, u_{k-3} (ghosts)
-      for (int k = 0; k < G; ++k) {
-        double u;
-        if (k == 0)
-          u = P1;
-        else if (k == 1)
-          u = dadd(P2, dmul(c.a1, u1));
-        else if (k == 2)
-          u = dadd(dadd(P3, dmul(c.a2, u2)), dmul(c.a1, u1));
-        else
-          u = dadd(dadd(dmul(c.a3, u3), dmul(c.a2, u2)), dmul(c.a1, u1));
-        u3 = u2;
-        u2 = u1;
-        u1 = u;
-        g[k] = dmul(c.b, u);  // v_{j+1+k}
-      }
-      double w1 = 0.0, w2 = 0.0, w3 = 0.0;  // u'_{k+1}, u'_{k+2}, u'_{k+3}
-      double s[3] = {0.0, 0.0, 0.0};
-      for (int k = G - 1; k >= 0; --k) {
-        const double u = dadd(dadd(dadd(g[k], dmul(c.a3, w3)), dmul(c.a2, w2)), dmul(c.a1, w1));
-        w3 = w2;
-        w2 = w1;
-        w1 = u;
-        if (k < 3) s[k] = u;
-      }
-      o[9 + 0 + m] = s[0];
-      o[9 + 3 + m] = s[1];
-      o[9 + 6 + m] = s[2];
-    }
-  }
-}
-
-// Bit-packed masks per direction: dir 0 words[(lev*ny+iy)*W + ix/64],
-// dir 1 words[(lev*nx+ix)*W + iy/64]; bit k = sea at line position k.
-__global__ void k_pack_bits(const uint8_t* mask, int dir, int64_t nx, int64_t ny, int64_t nlev,
-                            int64_t words, uint64_t* bits) {
-  const int64_t nlines = dir == 0 ? ny : nx;
-  const int64_t n = dir == 0 ? nx : ny;
-  const int64_t total = nlev * nlines * words;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t wi = t % words;
-    const int64_t ln = t / words;  // lev*nlines + line
-    const int64_t lev = ln / nlines, line = ln - lev * nlines;
-    uint64_t v = 0;
-    for (int b = 0; b < 64; ++b) {
-      const int64_t k = wi * 64 + b;
-      if (k >= n) break;
-      const int64_t idx = dir == 0 ? (lev * ny + line) * nx + k : (lev * ny + k) * nx + line;
-      if (mask[idx]) v |= (1ull << b);
-    }
-    bits[t] = v;
   }
 }
 
 template <typename T>
 int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
-  const int64_t nlines = a.dir == 0 ? a.ny : a.nx;
-  const int64_t total = a.nvar * a.nlev * nlines;
   const int threads = 128;
-  const int64_t blocks = (total + threads - 1) / threads;
-  if (a.dir == 0) {
+  const int64_t planes = a.nvar * a.nlev;
+  if (a.dir == 1) {
+    constexpr int L = 4, U = 4;
+    const int64_t total = ((planes + L - 1) / L) * a.nx;
+    const int64_t blocks = (total + threads - 1) / threads;
     if (a.transpose)
-      k_stream<T, 0, true><<<blocks, threads, 0, st>>>(in, out, a);
+      k_sweep_y<T, true, L, U><<<blocks, threads, 0, st>>>(in, out, a);
     else
-      k_stream<T, 0, false><<<blocks, threads, 0, st>>>(in, out, a);
+      k_sweep_y<T, false, L, U><<<blocks, threads, 0, st>>>(in, out, a);
   } else {
-    if (a.transpose)
-      k_stream<T, 1, true><<<blocks, threads, 0, st>>>(in, out, a);
-    else
-      k_stream<T, 1, false><<<blocks, threads, 0, st>>>(in, out, a);
+    const int64_t total = planes * a.ny;
+    const int64_t blocks = (total + threads - 1) / threads;
+    // 16 B vector access needs every row start 16 B aligned
+    const int64_t vec_elems = 16 / static_cast<int64_t>(sizeof(T));
+    const bool vec = (a.nx % vec_elems == 0) &&
+                     (reinterpret_cast<uintptr_t>(in) % 16 == 0) &&
+                     (reinterpret_cast<uintptr_t>(out) % 16 == 0);
+    if (vec) {
+      if (a.transpose)
+        k_sweep_x<T, true, true><<<blocks, threads, 0, st>>>(in, out, a);
+      else
+        k_sweep_x<T, false, true><<<blocks, threads, 0, st>>>(in, out, a);
+    } else {
+      if (a.transpose)
+        k_sweep_x<T, true, false><<<blocks, threads, 0, st>>>(in, out, a);
+      else
+        k_sweep_x<T, false, false><<<blocks, threads, 0, st>>>(in, out, a);
+    }
   }
   return 1;
 }
