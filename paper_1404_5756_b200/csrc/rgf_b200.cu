@@ -128,6 +128,7 @@ struct rgf_op {
   int64_t words[2] = {0, 0};
   DevBuf<int> cls_d;
   DevBuf<double> clos;  // [class][dir][nh][18]
+  DevBuf<double4> entry;  // [var][segments] anti-causal entry states (apply scratch)
   int nclass = 0;
   std::mutex mu;  // apply() is const in the reference; serialize buffer reuse
 
@@ -164,6 +165,11 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.ghost = op->ghost_d.p;
     a.cls = op->cls_d.p;
     a.clos = op->clos.p;
+    a.seg_off = d.seg_off.p;
+    a.segs = d.segs.p;
+    a.nsegs = d.nsegs;
+    op->entry.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs)));
+    a.entry = op->entry.p;
     a.pre_scale = pre;
     a.post_scale = post;
     op->launches += rgfb::launch_stream_sweep<T>(in, out, a, st);
@@ -551,7 +557,7 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
   return guarded([&] {
     if (!op || !out) throw InvalidArgument("device_bytes: null argument");
     uint64_t b = op->ghost_d.bytes() + op->variance.bytes() + op->in_d.bytes() +
-                 op->bits[0].bytes() + op->bits[1].bytes() + op->clos.bytes() + op->cls_d.bytes() +
+                 op->bits[0].bytes() + op->bits[1].bytes() + op->clos.bytes() + op->cls_d.bytes() + op->entry.bytes() +
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})
       b += d->c3.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes();
