@@ -21,6 +21,7 @@
 #include "setup_kernels.cuh"
 #include "sweep_generic.cuh"
 #include "sweep_stream.cuh"
+#include "sweep_bulk.cuh"
 #include "closures.cuh"
 
 namespace {

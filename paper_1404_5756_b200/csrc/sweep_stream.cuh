@@ -160,14 +160,9 @@ __global__ void __launch_bounds__(128) k_entries(const T* __restrict__ z, Stream
   const int64_t planes = a.nvar * a.nlev;
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (tid >= planes * nlines) return;
-  int64_t p, line;
-  if (DIR == 0) {  // plane-fastest (matches k_sweep_x)
-    line = tid / planes;
-    p = tid - line * planes;
-  } else {  // line-fastest (matches k_sweep_y)
-    p = tid / nlines;
-    line = tid - p * nlines;
-  }
+  // plane-fastest: the planes of one line share its closure rows in L2
+  const int64_t line = tid / planes;
+  const int64_t p = tid - line * planes;
   const int64_t var = p / a.nlev, lev = p - var * a.nlev;
   const int64_t hb = DIR == 0 ? line * a.nx : line;
   const T* zl = z + p * nh + hb;
@@ -540,13 +535,28 @@ __global__ void __launch_bounds__(128) k_x_pass_d(T* __restrict__ out, StreamArg
 }
 
 template <typename T>
+inline bool ybulk_supported(const T* in, const T* out, int64_t nx);
+template <typename T, bool TR, bool PD>
+void launch_ybulk(const T* in, T* out, const StreamArgs& a, cudaStream_t st);
+
+template <typename T>
 int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const int threads = 128;
   const int64_t planes = a.nvar * a.nlev;
   const int64_t nlines = a.dir == 0 ? a.ny : a.nx;
   const int64_t chains = planes * nlines;
   const int64_t eblocks = (chains + threads - 1) / threads;
-  if (a.dir == 1) {
+  if (a.dir == 1 && ybulk_supported(in, out, a.nx)) {
+    if (a.transpose) {
+      launch_ybulk<T, true, false>(in, out, a, st);
+      k_entries<T, 1, true><<<eblocks, threads, 0, st>>>(out, a);
+      launch_ybulk<T, true, true>(out, out, a, st);
+    } else {
+      launch_ybulk<T, false, false>(in, out, a, st);
+      k_entries<T, 1, false><<<eblocks, threads, 0, st>>>(out, a);
+      launch_ybulk<T, false, true>(out, out, a, st);
+    }
+  } else if (a.dir == 1) {
     constexpr int L = 4, U = 4;
     const int64_t total = ((planes + L - 1) / L) * a.nx;
     const int64_t blocks = (total + threads - 1) / threads;

@@ -49,12 +49,15 @@ def random_case(seed, nx=57, ny=43, nlev=3, sea=0.8, smin=1.2, smax=4.5):
 KINDS = ["GX", "GY", "GXT", "GYT", "V", "VT", "B", "GYGX"]
 
 
-@pytest.mark.parametrize("order,k", [(3, 1), (1, 1), (1, 5)])
-def test_all_kinds_fp64_random_masks(P, order, k):
-    g, rx, ry = random_case(10 + order + k)
-    var = np.random.default_rng(2).uniform(0.5, 2.0, (3, 43, 57))
+@pytest.mark.parametrize("order,k,nx", [(3, 1, 57), (3, 1, 58), (3, 1, 96), (1, 1, 57),
+                                        (1, 5, 57)])
+def test_all_kinds_fp64_random_masks(P, order, k, nx):
+    """nx=57: unaligned rows (register-batched kernels); nx=58/96: bulk-copy
+    y-sweep with a partial and a full last column tile."""
+    g, rx, ry = random_case(10 + order + k, nx=nx)
+    var = np.random.default_rng(2).uniform(0.5, 2.0, (3, 43, nx))
     gpu, cpu = build_pair(P, g, rx, ry, order=order, k=k, variance=var)
-    f = np.random.default_rng(3).standard_normal((2, 3, 43, 57))
+    f = np.random.default_rng(3).standard_normal((2, 3, 43, nx))
     for name in KINDS:
         kind = getattr(P, name)
         got = gpu.apply(kind, f)
@@ -64,11 +67,11 @@ def test_all_kinds_fp64_random_masks(P, order, k):
         assert np.all(got[:, land] == 0.0), name
 
 
-@pytest.mark.parametrize("order,k", [(3, 1), (1, 5)])
-def test_fp32_storage(P, order, k):
-    g, rx, ry = random_case(40 + order)
+@pytest.mark.parametrize("order,k,nx", [(3, 1, 57), (3, 1, 60), (1, 5, 57)])
+def test_fp32_storage(P, order, k, nx):
+    g, rx, ry = random_case(40 + order, nx=nx)
     gpu, cpu = build_pair(P, g, rx, ry, order=order, k=k)
-    f32 = np.random.default_rng(4).standard_normal((1, 3, 43, 57)).astype(np.float32)
+    f32 = np.random.default_rng(4).standard_normal((1, 3, 43, nx)).astype(np.float32)
     for name in ("GYGX", "VT", "B"):
         got = gpu.apply(getattr(P, name), f32)
         assert got.dtype == np.float32
@@ -267,6 +270,17 @@ def test_exact_mode_matches_oracle_to_rounding(P, monkeypatch):
         got = gpu.apply(getattr(P, name), f)
         want = cpu.apply(getattr(O, name), f)
         assert relmax(got, want) <= 1e-14, (name, relmax(got, want))
+
+
+def test_many_planes_partial_blocks(P):
+    """40 planes (2 vars x 20 levels): y-sweep CTAs with 16 and 8 planes."""
+    g, rx, ry = random_case(321, nx=64, ny=37, nlev=20, sea=0.75)
+    gpu, cpu = build_pair(P, g, rx, ry)
+    f = np.random.default_rng(6).standard_normal((2, 20, 37, 64))
+    for name in ("GYGX", "VT", "GY", "GYT"):
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
 
 
 def test_streaming_vs_exact_path(P, monkeypatch):
