@@ -538,6 +538,10 @@ template <typename T>
 inline bool ybulk_supported(const T* in, const T* out, int64_t nx);
 template <typename T, bool TR, bool PD>
 void launch_ybulk(const T* in, T* out, const StreamArgs& a, cudaStream_t st);
+template <typename T>
+inline bool xbulk_supported(const T* in, const T* out, int64_t nx, int64_t planes);
+template <typename T, bool TR, bool PD>
+void launch_xbulk(const T* in, T* out, const StreamArgs& a, cudaStream_t st);
 
 template <typename T>
 int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
@@ -568,6 +572,16 @@ int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t s
       k_y_pass_a<T, false, L, U><<<blocks, threads, 0, st>>>(in, out, a);
       k_entries<T, 1, false><<<eblocks, threads, 0, st>>>(out, a);
       k_y_pass_d<T, false, L, U><<<blocks, threads, 0, st>>>(out, a);
+    }
+  } else if (xbulk_supported(in, out, a.nx, planes)) {
+    if (a.transpose) {
+      launch_xbulk<T, true, false>(in, out, a, st);
+      k_entries<T, 0, true><<<eblocks, threads, 0, st>>>(out, a);
+      launch_xbulk<T, true, true>(out, out, a, st);
+    } else {
+      launch_xbulk<T, false, false>(in, out, a, st);
+      k_entries<T, 0, false><<<eblocks, threads, 0, st>>>(out, a);
+      launch_xbulk<T, false, true>(out, out, a, st);
     }
   } else {
     const int64_t blocks = (chains + threads - 1) / threads;
