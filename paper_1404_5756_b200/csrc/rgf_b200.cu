@@ -21,7 +21,7 @@
 #include "setup_kernels.cuh"
 #include "sweep_generic.cuh"
 #include "sweep_stream.cuh"
-#include "sweep_bulk.cuh"
+#include "sweep_tma.cuh"
 #include "closures.cuh"
 
 namespace {
@@ -173,7 +173,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.entry = op->entry.p;
     a.pre_scale = pre;
     a.post_scale = post;
-    op->launches += rgfb::launch_stream_sweep<T>(in, out, a, st);
+    op->launches += static_cast<unsigned long long>(rgfb::launch_stream_sweep<T>(in, out, a, st));
     CUDA_OK(cudaGetLastError());
     return;
   }

@@ -535,13 +535,9 @@ __global__ void __launch_bounds__(128) k_x_pass_d(T* __restrict__ out, StreamArg
 }
 
 template <typename T>
-inline bool ybulk_supported(const T* in, const T* out, int64_t nx);
-template <typename T, bool TR, bool PD>
-void launch_ybulk(const T* in, T* out, const StreamArgs& a, cudaStream_t st);
+inline bool tma_supported(const T* in, const T* out, int64_t nx);
 template <typename T>
-inline bool xbulk_supported(const T* in, const T* out, int64_t nx, int64_t planes);
-template <typename T, bool TR, bool PD>
-void launch_xbulk(const T* in, T* out, const StreamArgs& a, cudaStream_t st);
+int launch_tma_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st);
 
 template <typename T>
 int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
@@ -550,17 +546,8 @@ int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t s
   const int64_t nlines = a.dir == 0 ? a.ny : a.nx;
   const int64_t chains = planes * nlines;
   const int64_t eblocks = (chains + threads - 1) / threads;
-  if (a.dir == 1 && ybulk_supported(in, out, a.nx)) {
-    if (a.transpose) {
-      launch_ybulk<T, true, false>(in, out, a, st);
-      k_entries<T, 1, true><<<eblocks, threads, 0, st>>>(out, a);
-      launch_ybulk<T, true, true>(out, out, a, st);
-    } else {
-      launch_ybulk<T, false, false>(in, out, a, st);
-      k_entries<T, 1, false><<<eblocks, threads, 0, st>>>(out, a);
-      launch_ybulk<T, false, true>(out, out, a, st);
-    }
-  } else if (a.dir == 1) {
+  if (tma_supported(in, out, a.nx)) return launch_tma_sweep<T>(in, out, a, st);
+  if (a.dir == 1) {
     constexpr int L = 4, U = 4;
     const int64_t total = ((planes + L - 1) / L) * a.nx;
     const int64_t blocks = (total + threads - 1) / threads;
@@ -572,16 +559,6 @@ int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t s
       k_y_pass_a<T, false, L, U><<<blocks, threads, 0, st>>>(in, out, a);
       k_entries<T, 1, false><<<eblocks, threads, 0, st>>>(out, a);
       k_y_pass_d<T, false, L, U><<<blocks, threads, 0, st>>>(out, a);
-    }
-  } else if (xbulk_supported(in, out, a.nx, planes)) {
-    if (a.transpose) {
-      launch_xbulk<T, true, false>(in, out, a, st);
-      k_entries<T, 0, true><<<eblocks, threads, 0, st>>>(out, a);
-      launch_xbulk<T, true, true>(out, out, a, st);
-    } else {
-      launch_xbulk<T, false, false>(in, out, a, st);
-      k_entries<T, 0, false><<<eblocks, threads, 0, st>>>(out, a);
-      launch_xbulk<T, false, true>(out, out, a, st);
     }
   } else {
     const int64_t blocks = (chains + threads - 1) / threads;

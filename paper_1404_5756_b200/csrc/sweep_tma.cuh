@@ -1,0 +1,534 @@
+// TMA-fed producer/consumer sweeps for the 3rd-RF (forward G_dir and adjoint
+// G_dir^T), used whenever rows are 16 B aligned.
+//
+// Pass A (ascending) and pass D (descending) are separate kernels; each has
+// one producer warp that streams U-element stages of every chain of the CTA
+// into an S-deep shared-memory ring with TMA tensor loads (one instruction
+// per box; the TMA engine zero-fills out-of-range rows/planes), and consumer
+// warps whose lanes each advance one chain.
+//
+// Segment ends are handled without a separate kernel: pass A writes the raw
+// 3-value causal state of every chain at every segment end j (forward:
+// p_j, p_{j-1}, p_{j-2}; adjoint: the pending causal-transpose contributions
+// into the first three ghosts) to `state[var][segment]`. Pass D keeps the next
+// segment's raw state, its right-ghost closure matrix (closures.cuh) and the
+// descriptor after it in flight, so entering a segment is a 3x3 product on
+// registers (covariance.cpp:271-273 + rf3.hpp:232-261 collapsed, see
+// sweep_stream.cuh).
+//
+// y-sweep (lines = columns): a CTA owns a 32-column tile and NW planes; the
+//   field box is [NW planes x U rows x 32 columns], coefficients one
+//   [U rows x 32 columns] box shared by all NW planes; lanes = columns, so
+//   smem reads are conflict-free and stores are coalesced 256 B st.global.
+// x-sweep (lines = rows): a CTA owns one row and 32*NW planes; the field box
+//   is [U x-positions x 32*NW planes] with 128 B swizzle (lanes = planes
+//   read 16 B chunks without bank conflicts), coefficients a [U] row segment
+//   broadcast to every lane; results are written back in place and returned
+//   with one TMA tensor store per stage.
+#pragma once
+#include "async_copy.cuh"
+#include "sweep_stream.cuh"
+#include "tma.cuh"
+
+namespace rgfb {
+
+// ---------------------------------------------------------------- helpers
+// Next-segment prefetch for pass D: (descriptor two ahead) -> (closure
+// matrix, raw state one ahead).
+struct SegPrefetch {
+  int64_t sidx, sfirst;  // current segment (the next one to be entered)
+  int2 seg_next;         // descriptor of segment sidx-1
+  double4 raw;           // raw state of segment sidx
+  double M[9];           // closure of segment sidx's end
+  int64_t jend;          // end position of segment sidx
+};
+
+template <bool TR>
+__device__ __forceinline__ void pf_load(SegPrefetch& f, const int2* segs, const double4* raw,
+                                        const double* CLline, int64_t stride, int64_t n, int G) {
+  // assumes f.sidx >= f.sfirst and jend set
+  f.raw = raw[f.sidx];
+  const bool ghost = f.jend < n - 1 && G > 0;
+  const double* M = CLline + f.jend * stride * 18 + (TR ? 9 : 0);
+#pragma unroll
+  for (int q = 0; q < 9; ++q) f.M[q] = ghost ? __ldg(M + q) : 0.0;
+  f.seg_next = f.sidx - 1 >= f.sfirst ? __ldg(segs + f.sidx - 1) : make_int2(0, 0);
+}
+
+template <bool TR>
+__device__ __forceinline__ void pf_init(SegPrefetch& f, int64_t s0, int64_t s1, const int2* segs,
+                                        const double4* raw, const double* CLline, int64_t stride,
+                                        int64_t n, int G) {
+  f.sfirst = s0;
+  f.sidx = s1 - 1;
+  f.jend = -1;
+  if (f.sidx >= f.sfirst) {
+    const int2 sg = __ldg(segs + f.sidx);
+    f.jend = sg.x + sg.y - 1;
+    pf_load<TR>(f, segs, raw, CLline, stride, n, G);
+  }
+}
+
+// entry state of the current segment, then advance the prefetch
+template <bool TR>
+__device__ __forceinline__ double4 pf_take(SegPrefetch& f, const int2* segs, const double4* raw,
+                                           const double* CLline, int64_t stride, int64_t n,
+                                           int G) {
+  const double x0 = f.raw.x, x1 = f.raw.y, x2 = f.raw.z;
+  double4 e;
+  e.x = fma(f.M[0], x0, fma(f.M[1], x1, f.M[2] * x2));
+  e.y = fma(f.M[3], x0, fma(f.M[4], x1, f.M[5] * x2));
+  e.z = fma(f.M[6], x0, fma(f.M[7], x1, f.M[8] * x2));
+  e.w = 0.0;
+  --f.sidx;
+  if (f.sidx >= f.sfirst) {
+    f.jend = f.seg_next.x + f.seg_next.y - 1;
+    pf_load<TR>(f, segs, raw, CLline, stride, n, G);
+  }
+  return e;
+}
+
+// raw state written by pass A at a segment end
+__device__ __forceinline__ double4 raw_state(const FwdA& s) {
+  return make_double4(s.p1, s.p2, s.p3, 0.0);
+}
+__device__ __forceinline__ double4 raw_state(const AdjA& s) {
+  return make_double4(fma(s.x1, s.u1, s.y33 + s.y22), s.y32 + s.y21, s.y31, 0.0);
+}
+
+// mask word window: bits of positions [64w, 64w+64) and the next word
+struct MaskWin {
+  int64_t w = -2;
+  uint64_t cur = 0, nxt = 0;
+  __device__ __forceinline__ void at(const uint64_t* W, int64_t k, int64_t words, bool desc) {
+    const int64_t wi = k >> 6;
+    if (wi == w) return;
+    const int64_t wn = desc ? wi - 1 : wi + 1;
+    if ((desc ? wi == w - 1 : wi == w + 1)) {
+      cur = nxt;
+    } else {
+      cur = ldw(W, wi);
+    }
+    nxt = (wn >= 0 && wn < words) ? ldw(W, wn) : 0ull;
+    w = wi;
+  }
+  __device__ __forceinline__ int bit(int64_t k) const { return int((cur >> (k & 63)) & 1ull); }
+  // sea(k+1) for the ascending pass
+  __device__ __forceinline__ int bit_next(int64_t k) const {
+    return (k & 63) == 63 ? int(nxt & 1ull) : int((cur >> ((k & 63) + 1)) & 1ull);
+  }
+};
+
+// ================================================================ y-sweep
+template <typename T, int NW, int U>
+struct YT {
+  static constexpr size_t field = size_t(NW) * U * 32 * sizeof(T);
+  static constexpr size_t coef = size_t(U) * 32 * sizeof(Coef3);
+  static constexpr size_t idc = size_t(U) * 32 * sizeof(double);
+  static constexpr size_t bytes = field + coef + idc;
+};
+
+template <typename T, bool TR, bool PD, int NW, int U, int S>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    k_ytma(T* __restrict__ out, StreamArgs a, const __grid_constant__ CUtensorMap tm_field,
+           const __grid_constant__ CUtensorMap tm_coef, const __grid_constant__ CUtensorMap tm_idc) {
+  using L = YT<T, NW, U>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::bytes);
+  uint64_t* empty = full + S;
+
+  const int64_t nx = a.nx, ny = a.ny, nh = nx * ny;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t PB = (planes + NW - 1) / NW;
+  const int64_t tile = blockIdx.x / PB;
+  const int64_t p0 = (blockIdx.x - tile * PB) * NW;
+  const int64_t ix0 = tile * 32;
+  const int ncol = static_cast<int>(nx - ix0 < 32 ? nx - ix0 : 32);
+  const int nwp = static_cast<int>(planes - p0 < NW ? planes - p0 : NW);
+  const bool need_idc = a.idc != nullptr && (PD ? !TR : TR);
+  const int64_t nst = (ny + U - 1) / U;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], nwp);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto lo_of = [&](int64_t i) -> int64_t { return PD ? ny - (i + 1) * U : i * U; };
+
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_field);
+      tma_prefetch_desc(&tm_coef);
+      if (need_idc) tma_prefetch_desc(&tm_idc);
+      const uint32_t total = static_cast<uint32_t>(L::field + L::coef + (need_idc ? L::idc : 0));
+      for (int64_t i = 0; i < nst; ++i) {
+        const int s = static_cast<int>(i % S);
+        const int64_t m = i / S;
+        if (m > 0) mbar_wait(&empty[s], static_cast<uint32_t>((m - 1) & 1));
+        const int lo = static_cast<int>(lo_of(i));
+        unsigned char* base = smem + s * L::bytes;
+        mbar_arrive_expect_tx(&full[s], total);
+        tma_load_3d(base, &tm_field, static_cast<int>(ix0), lo, static_cast<int>(p0), &full[s]);
+        tma_load_2d(base + L::field, &tm_coef, static_cast<int>(4 * ix0), lo, &full[s]);
+        if (need_idc)
+          tma_load_2d(base + L::field + L::coef, &tm_idc, static_cast<int>(ix0), lo, &full[s]);
+      }
+    }
+    return;
+  }
+  if (warp >= nwp) return;
+
+  // consumer: chain (plane p0+warp, column ix0+lane)
+  const int64_t p = p0 + warp;
+  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
+  const bool act = lane < ncol;
+  const int64_t ix = ix0 + (act ? lane : 0);
+  T* dst = out + p * nh + ix;
+  const uint64_t* W = a.bits + (lev * nx + ix) * a.words;
+  const double* PRE = (!PD && TR && a.pre_scale) ? a.pre_scale + lev * nh + ix : nullptr;
+  const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + ix : nullptr;
+  double4* RAW = a.entry + var * a.nsegs;
+  const int64_t s0 = a.seg_off[lev * nx + ix], s1 = a.seg_off[lev * nx + ix + 1];
+  const int G = a.ghost[lev];
+  const double* CLline = a.clos + ((int64_t)(a.cls[lev] * 2 + 1) * nh + ix) * 18;
+  MaskWin mw;
+
+  typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
+                            typename std::conditional<TR, AdjA, FwdA>::type>::type st;
+  SegPrefetch pf;
+  int64_t sA = s0;  // pass A: next segment index to be closed
+  int nxt = 0;
+  if constexpr (PD) pf_init<TR>(pf, s0, s1, a.segs, RAW, CLline, nx, ny, G);
+
+  for (int64_t i = 0; i < nst; ++i) {
+    const int s = static_cast<int>(i % S);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
+    const int64_t lo = lo_of(i);
+    const unsigned char* base = smem + s * L::bytes;
+    const T* fld = reinterpret_cast<const T*>(base) + warp * U * 32 + lane;
+    const Coef3* cf = reinterpret_cast<const Coef3*>(base + L::field) + lane;
+    const double* id = reinterpret_cast<const double*>(base + L::field + L::coef) + lane;
+    if constexpr (!PD) {
+      const int nr = static_cast<int>(ny - lo < U ? ny - lo : U);
+      for (int r = 0; r < nr; ++r) {
+        const int64_t k = lo + r;
+        mw.at(W, k, a.words, false);
+        const int sea = mw.bit(k);
+        double w = static_cast<double>(fld[r * 32]);
+        if (TR) {
+          if (PRE) w *= __ldg(PRE + k * nx);
+          if (need_idc) w *= id[r * 32];
+        }
+        const double res = st.step(cf[r * 32], w, sea);
+        if (act) dst[k * nx] = static_cast<T>(res);
+        if (sea && !mw.bit_next(k)) {  // segment end: raw closure input
+          if (act) RAW[sA] = raw_state(st);
+          ++sA;
+        }
+      }
+    } else {
+      const int rmin = static_cast<int>(lo < 0 ? -lo : 0);
+      for (int r = U - 1; r >= rmin; --r) {
+        const int64_t k = lo + r;
+        mw.at(W, k, a.words, true);
+        const int sea = mw.bit(k);
+        const Coef3 c = cf[r * 32];
+        if (sea && !nxt) st.enter(pf_take<TR>(pf, a.segs, RAW, CLline, nx, ny, G), c);
+        double o = st.step(c, static_cast<double>(fld[r * 32]));
+        if (!TR && need_idc) o *= id[r * 32];
+        if (POST) o *= __ldg(POST + k * nx);
+        if (act) dst[k * nx] = static_cast<T>(sea ? o : 0.0);
+        nxt = sea;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+constexpr int kYtNW = 16, kYtU = 8, kYtS = 4;
+
+// ================================================================ x-sweep
+// one row, up to 32*NW planes per CTA; U*sizeof(T) = 128 B (swizzle atom)
+template <typename T, int NW>
+struct XT {
+  static constexpr int U = 128 / int(sizeof(T));
+  static constexpr size_t field = size_t(NW) * 32 * 128;
+  static constexpr size_t coef = size_t(U) * sizeof(Coef3);
+  static constexpr size_t idc = size_t(U) * sizeof(double);
+  static constexpr size_t bytes = (field + coef + idc + 1023) / 1024 * 1024;
+};
+
+// byte offset of element u of plane-row r in a 128B-swizzled [rows][128 B] tile
+__device__ __forceinline__ uint32_t swz128(int r, uint32_t byte_in_row) {
+  return static_cast<uint32_t>(r) * 128u + ((((byte_in_row >> 4) ^ (r & 7)) << 4) | (byte_in_row & 15u));
+}
+
+template <typename T, bool TR, bool PD, int NW, int S>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    k_xtma(T* __restrict__ out, StreamArgs a, const __grid_constant__ CUtensorMap tm_in,
+           const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ CUtensorMap tm_coef,
+           const __grid_constant__ CUtensorMap tm_idc) {
+  using L = XT<T, NW>;
+  constexpr int U = L::U;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::bytes);
+  uint64_t* empty = full + S;
+
+  const int64_t n = a.nx, ny = a.ny, nh = n * ny;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
+  const int64_t iy = blockIdx.x / PB;
+  const int64_t p0 = (blockIdx.x - iy * PB) * 32 * NW;
+  const int npl = static_cast<int>(planes - p0 < 32 * NW ? planes - p0 : 32 * NW);
+  const int nwp = (npl + 31) / 32;
+  const bool need_idc = a.idc != nullptr && (PD ? !TR : TR);
+  const int64_t nst = (n + U - 1) / U;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto k0_of = [&](int64_t i) -> int64_t { return (PD ? nst - 1 - i : i) * U; };
+
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      tma_prefetch_desc(&tm_in);
+      tma_prefetch_desc(&tm_coef);
+      const uint32_t total = static_cast<uint32_t>(L::field + L::coef + (need_idc ? L::idc : 0));
+      for (int64_t i = 0; i < nst; ++i) {
+        const int s = static_cast<int>(i % S);
+        const int64_t m = i / S;
+        if (m > 0) mbar_wait(&empty[s], static_cast<uint32_t>((m - 1) & 1));
+        const int k0 = static_cast<int>(k0_of(i));
+        unsigned char* base = smem + s * L::bytes;
+        mbar_arrive_expect_tx(&full[s], total);
+        tma_load_3d(base, &tm_in, k0, static_cast<int>(iy), static_cast<int>(p0), &full[s]);
+        tma_load_2d(base + L::field, &tm_coef, 4 * k0, static_cast<int>(iy), &full[s]);
+        if (need_idc)
+          tma_load_2d(base + L::field + L::coef, &tm_idc, k0, static_cast<int>(iy), &full[s]);
+      }
+    }
+    return;
+  }
+
+  // consumers: lane = plane p0 + 32*warp + lane of row iy
+  const int pr = warp * 32 + lane;  // row of the smem tile
+  const bool act = pr < npl;
+  const int64_t p = p0 + (act ? pr : 0);
+  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
+  const uint64_t* W = a.bits + (lev * ny + iy) * a.words;
+  const double* PRE = (!PD && TR && a.pre_scale) ? a.pre_scale + lev * nh + iy * n : nullptr;
+  const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + iy * n : nullptr;
+  double4* RAW = a.entry + var * a.nsegs;
+  const int64_t s0 = a.seg_off[lev * ny + iy], s1 = a.seg_off[lev * ny + iy + 1];
+  const int G = a.ghost[lev];
+  const double* CLline = a.clos + ((int64_t)(a.cls[lev] * 2 + 0) * nh + iy * n) * 18;
+  MaskWin mw;
+  typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
+                            typename std::conditional<TR, AdjA, FwdA>::type>::type st;
+  SegPrefetch pf;
+  int64_t sA = s0;
+  int nxt = 0;
+  if constexpr (PD) pf_init<TR>(pf, s0, s1, a.segs, RAW, CLline, 1, n, G);
+
+  for (int64_t i = 0; i < nst; ++i) {
+    const int s = static_cast<int>(i % S);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
+    const int64_t k0 = k0_of(i);
+    const int nk = static_cast<int>(n - k0 < U ? n - k0 : U);
+    unsigned char* base = smem + s * L::bytes;
+    const Coef3* cf = reinterpret_cast<const Coef3*>(base + L::field);
+    const double* id = reinterpret_cast<const double*>(base + L::field + L::coef);
+    // this lane's U elements (128 B) through the swizzle, 16 B at a time
+    constexpr int EPC = 16 / int(sizeof(T));  // elements per 16 B chunk
+    double v[U];
+#pragma unroll
+    for (int q = 0; q < U / EPC; ++q) {
+      const uint32_t off = swz128(pr, q * 16);
+      if constexpr (sizeof(T) == 8) {
+        const double2 t = *reinterpret_cast<const double2*>(base + off);
+        v[2 * q] = t.x;
+        v[2 * q + 1] = t.y;
+      } else {
+        const float4 t = *reinterpret_cast<const float4*>(base + off);
+        v[4 * q] = t.x;
+        v[4 * q + 1] = t.y;
+        v[4 * q + 2] = t.z;
+        v[4 * q + 3] = t.w;
+      }
+    }
+    if constexpr (!PD) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (u < nk) {
+          const int64_t k = k0 + u;
+          mw.at(W, k, a.words, false);
+          const int sea = mw.bit(k);
+          double w = v[u];
+          if (TR) {
+            if (PRE) w *= __ldg(PRE + k);
+            if (need_idc) w *= id[u];
+          }
+          v[u] = st.step(cf[u], w, sea);
+          if (sea && !mw.bit_next(k)) {
+            if (act) RAW[sA] = raw_state(st);
+            ++sA;
+          }
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = U - 1; u >= 0; --u) {
+        if (u < nk) {
+          const int64_t k = k0 + u;
+          mw.at(W, k, a.words, true);
+          const int sea = mw.bit(k);
+          const Coef3 c = cf[u];
+          if (sea && !nxt) st.enter(pf_take<TR>(pf, a.segs, RAW, CLline, 1, n, G), c);
+          double o = st.step(c, v[u]);
+          if (!TR && need_idc) o *= id[u];
+          if (POST) o *= __ldg(POST + k);
+          v[u] = sea ? o : 0.0;
+          nxt = sea;
+        }
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < U / EPC; ++q) {
+      const uint32_t off = swz128(pr, q * 16);
+      if constexpr (sizeof(T) == 8) {
+        *reinterpret_cast<double2*>(base + off) = make_double2(v[2 * q], v[2 * q + 1]);
+      } else {
+        *reinterpret_cast<float4*>(base + off) =
+            make_float4(static_cast<float>(v[4 * q]), static_cast<float>(v[4 * q + 1]),
+                        static_cast<float>(v[4 * q + 2]), static_cast<float>(v[4 * q + 3]));
+      }
+    }
+    // all consumers' results in smem -> one TMA store of the box
+    fence_proxy_async_smem();
+    asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NW) : "memory");
+    if (threadIdx.x == 0) {
+      tma_store_3d(&tm_out, static_cast<int>(k0), static_cast<int>(iy), static_cast<int>(p0), base);
+      bulk_commit();
+      // the stage is free once the store has read it (the previous stage's
+      // store is older; wait for it before releasing that stage)
+      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      if (i > 0) mbar_arrive(&empty[(i - 1) % S]);
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+constexpr int kXtNW = 4, kXtS = 4;
+
+// ------------------------------------------------------------- launchers
+template <typename T>
+inline bool tma_supported(const T* in, const T* out, int64_t nx) {
+  return (nx * static_cast<int64_t>(sizeof(T))) % 16 == 0 &&
+         reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
+}
+
+template <typename T, bool TR, bool PD>
+void launch_ytma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+  constexpr int NW = kYtNW, U = kYtU, S = kYtS;
+  const size_t smem = S * YT<T, NW, U>::bytes + 2 * S * sizeof(uint64_t) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_ytma<T, TR, PD, NW, U, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  const int64_t planes = a.nvar * a.nlev;
+  const uint64_t sz = sizeof(T);
+  const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
+  const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
+  const uint32_t fb[3] = {32, U, NW};
+  const CUtensorMap tf = make_tmap(PD ? static_cast<const void*>(out) : in, tma_dtype<T>(), 3, fd,
+                                   fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const uint64_t cd[2] = {uint64_t(4 * a.nx), uint64_t(a.ny)};
+  const uint64_t cs[1] = {uint64_t(4 * a.nx) * 8};
+  const uint32_t cb[2] = {128, U};
+  const CUtensorMap tc = make_tmap(a.c3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb,
+                                   CU_TENSOR_MAP_SWIZZLE_NONE);
+  const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
+  const uint64_t is[1] = {uint64_t(a.nx) * 8};
+  const uint32_t ib[2] = {32, U};
+  const CUtensorMap ti = a.idc ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+                                           CU_TENSOR_MAP_SWIZZLE_NONE)
+                               : tc;
+  const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NW - 1) / NW);
+  k_ytma<T, TR, PD, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tf, tc, ti);
+}
+
+template <typename T, bool TR, bool PD>
+void launch_xtma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+  constexpr int NW = kXtNW, S = kXtS;
+  using L = XT<T, NW>;
+  const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_xtma<T, TR, PD, NW, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(smem));
+    attr = true;
+  }
+  const int64_t planes = a.nvar * a.nlev;
+  const uint64_t sz = sizeof(T);
+  const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
+  const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
+  const uint32_t fb[3] = {uint32_t(L::U), 1, uint32_t(32 * NW)};
+  const CUtensorMap tin = make_tmap(PD ? static_cast<const void*>(out) : in, tma_dtype<T>(), 3,
+                                    fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B);
+  const CUtensorMap tout = make_tmap(out, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B);
+  const uint64_t cd[2] = {uint64_t(4 * a.nx), uint64_t(a.ny)};
+  const uint64_t cs[1] = {uint64_t(4 * a.nx) * 8};
+  const uint32_t cb[2] = {uint32_t(4 * L::U), 1};
+  const CUtensorMap tc = make_tmap(a.c3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb,
+                                   CU_TENSOR_MAP_SWIZZLE_NONE);
+  const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
+  const uint64_t is[1] = {uint64_t(a.nx) * 8};
+  const uint32_t ib[2] = {uint32_t(L::U), 1};
+  const CUtensorMap ti = a.idc ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+                                           CU_TENSOR_MAP_SWIZZLE_NONE)
+                               : tc;
+  const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
+  const int64_t blocks = a.ny * PB;
+  k_xtma<T, TR, PD, NW, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tin, tout, tc, ti);
+}
+
+template <typename T>
+int launch_tma_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+  if (a.dir == 1) {
+    if (a.transpose) {
+      launch_ytma<T, true, false>(in, out, a, st);
+      launch_ytma<T, true, true>(out, out, a, st);
+    } else {
+      launch_ytma<T, false, false>(in, out, a, st);
+      launch_ytma<T, false, true>(out, out, a, st);
+    }
+  } else {
+    if (a.transpose) {
+      launch_xtma<T, true, false>(in, out, a, st);
+      launch_xtma<T, true, true>(out, out, a, st);
+    } else {
+      launch_xtma<T, false, false>(in, out, a, st);
+      launch_xtma<T, false, true>(out, out, a, st);
+    }
+  }
+  return 2;
+}
+
+}  // namespace rgfb
