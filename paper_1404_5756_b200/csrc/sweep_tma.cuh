@@ -33,59 +33,68 @@
 namespace rgfb {
 
 // ---------------------------------------------------------------- helpers
-// Next-segment prefetch for pass D: (descriptor two ahead) -> (closure
-// matrix, raw state one ahead).
-struct SegPrefetch {
-  int64_t sidx, sfirst;  // current segment (the next one to be entered)
-  int2 seg_next;         // descriptor of segment sidx-1
-  double4 raw;           // raw state of segment sidx
-  double M[9];           // closure of segment sidx's end
-  int64_t jend;          // end position of segment sidx
+// Pass D consumes the entry states of its segments in reverse order; a
+// 3-deep register ring keeps the next three in flight so a short segment
+// never waits for its entry.
+struct EntryQ {
+  int64_t next, first;  // index of the next entry to fetch into the ring
+  double3 q0, q1, q2;
+  __device__ __forceinline__ double3 ld(const double4* E, int64_t i) const {
+    if (i < first) return make_double3(0.0, 0.0, 0.0);
+    const double2 a = *reinterpret_cast<const double2*>(E + i);
+    const double b = reinterpret_cast<const double*>(E + i)[2];
+    return make_double3(a.x, a.y, b);
+  }
+  __device__ __forceinline__ void init(const double4* E, int64_t s0, int64_t s1) {
+    first = s0;
+    q0 = ld(E, s1 - 1);
+    q1 = ld(E, s1 - 2);
+    q2 = ld(E, s1 - 3);
+    next = s1 - 4;
+  }
+  __device__ __forceinline__ double4 take(const double4* E) {
+    const double4 e = make_double4(q0.x, q0.y, q0.z, 0.0);
+    q0 = q1;
+    q1 = q2;
+    q2 = ld(E, next);
+    --next;
+    return e;
+  }
 };
 
-template <bool TR>
-__device__ __forceinline__ void pf_load(SegPrefetch& f, const int2* segs, const double4* raw,
-                                        const double* CLline, int64_t stride, int64_t n, int G) {
-  // assumes f.sidx >= f.sfirst and jend set
-  f.raw = raw[f.sidx];
-  const bool ghost = f.jend < n - 1 && G > 0;
-  const double* M = CLline + f.jend * stride * 18 + (TR ? 9 : 0);
-#pragma unroll
-  for (int q = 0; q < 9; ++q) f.M[q] = ghost ? __ldg(M + q) : 0.0;
-  f.seg_next = f.sidx - 1 >= f.sfirst ? __ldg(segs + f.sidx - 1) : make_int2(0, 0);
-}
-
-template <bool TR>
-__device__ __forceinline__ void pf_init(SegPrefetch& f, int64_t s0, int64_t s1, const int2* segs,
-                                        const double4* raw, const double* CLline, int64_t stride,
-                                        int64_t n, int G) {
-  f.sfirst = s0;
-  f.sidx = s1 - 1;
-  f.jend = -1;
-  if (f.sidx >= f.sfirst) {
-    const int2 sg = __ldg(segs + f.sidx);
-    f.jend = sg.x + sg.y - 1;
-    pf_load<TR>(f, segs, raw, CLline, stride, n, G);
+// Closure application between pass A and pass D: raw segment-end state ->
+// anti-causal entry state, in place, one thread per (line, plane) with
+// planes fastest so the planes of one line share the closure rows in L2.
+template <int DIR, bool TR>
+__global__ void __launch_bounds__(128) k_close(StreamArgs a) {
+  const int64_t n = DIR == 0 ? a.nx : a.ny;
+  const int64_t nlines = DIR == 0 ? a.ny : a.nx;
+  const int64_t nh = a.nx * a.ny;
+  const int64_t stride = DIR == 0 ? 1 : a.nx;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (tid >= planes * nlines) return;
+  const int64_t line = tid / planes;
+  const int64_t p = tid - line * planes;
+  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
+  const int64_t hb = DIR == 0 ? line * a.nx : line;
+  const int G = a.ghost[lev];
+  const double* CL = a.clos + ((int64_t)(a.cls[lev] * 2 + DIR) * nh + hb) * 18 + (TR ? 9 : 0);
+  const int64_t s0 = a.seg_off[lev * nlines + line], s1 = a.seg_off[lev * nlines + line + 1];
+  double4* E = a.entry + var * a.nsegs;
+  for (int64_t s = s0; s < s1; ++s) {
+    const int2 sg = __ldg(a.segs + s);
+    const int64_t j = sg.x + sg.y - 1;
+    double4 e = make_double4(0.0, 0.0, 0.0, 0.0);
+    if (j < n - 1 && G > 0) {
+      const double4 r = E[s];
+      const double* M = CL + j * stride * 18;
+      e.x = fma(__ldg(M + 0), r.x, fma(__ldg(M + 1), r.y, __ldg(M + 2) * r.z));
+      e.y = fma(__ldg(M + 3), r.x, fma(__ldg(M + 4), r.y, __ldg(M + 5) * r.z));
+      e.z = fma(__ldg(M + 6), r.x, fma(__ldg(M + 7), r.y, __ldg(M + 8) * r.z));
+    }
+    E[s] = e;
   }
-}
-
-// entry state of the current segment, then advance the prefetch
-template <bool TR>
-__device__ __forceinline__ double4 pf_take(SegPrefetch& f, const int2* segs, const double4* raw,
-                                           const double* CLline, int64_t stride, int64_t n,
-                                           int G) {
-  const double x0 = f.raw.x, x1 = f.raw.y, x2 = f.raw.z;
-  double4 e;
-  e.x = fma(f.M[0], x0, fma(f.M[1], x1, f.M[2] * x2));
-  e.y = fma(f.M[3], x0, fma(f.M[4], x1, f.M[5] * x2));
-  e.z = fma(f.M[6], x0, fma(f.M[7], x1, f.M[8] * x2));
-  e.w = 0.0;
-  --f.sidx;
-  if (f.sidx >= f.sfirst) {
-    f.jend = f.seg_next.x + f.seg_next.y - 1;
-    pf_load<TR>(f, segs, raw, CLline, stride, n, G);
-  }
-  return e;
 }
 
 // raw state written by pass A at a segment end
@@ -163,6 +172,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 
   if (warp == NW) {  // producer
     if (lane == 0) {
+      const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
       tma_prefetch_desc(&tm_field);
       tma_prefetch_desc(&tm_coef);
       if (need_idc) tma_prefetch_desc(&tm_idc);
@@ -174,10 +184,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         const int lo = static_cast<int>(lo_of(i));
         unsigned char* base = smem + s * L::bytes;
         mbar_arrive_expect_tx(&full[s], total);
-        tma_load_3d(base, &tm_field, static_cast<int>(ix0), lo, static_cast<int>(p0), &full[s]);
-        tma_load_2d(base + L::field, &tm_coef, static_cast<int>(4 * ix0), lo, &full[s]);
+        tma_load_3d(base, &tm_field, static_cast<int>(ix0), lo, static_cast<int>(p0), &full[s],
+                    pol_stream);
+        tma_load_2d(base + L::field, &tm_coef, static_cast<int>(4 * ix0), lo, &full[s], pol_keep);
         if (need_idc)
-          tma_load_2d(base + L::field + L::coef, &tm_idc, static_cast<int>(ix0), lo, &full[s]);
+          tma_load_2d(base + L::field + L::coef, &tm_idc, static_cast<int>(ix0), lo, &full[s],
+                      pol_keep);
       }
     }
     return;
@@ -195,16 +207,14 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + ix : nullptr;
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * nx + ix], s1 = a.seg_off[lev * nx + ix + 1];
-  const int G = a.ghost[lev];
-  const double* CLline = a.clos + ((int64_t)(a.cls[lev] * 2 + 1) * nh + ix) * 18;
   MaskWin mw;
 
   typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
                             typename std::conditional<TR, AdjA, FwdA>::type>::type st;
-  SegPrefetch pf;
+  EntryQ eq;
   int64_t sA = s0;  // pass A: next segment index to be closed
   int nxt = 0;
-  if constexpr (PD) pf_init<TR>(pf, s0, s1, a.segs, RAW, CLline, nx, ny, G);
+  if constexpr (PD) eq.init(RAW, s0, s1);
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
@@ -226,7 +236,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
           if (need_idc) w *= id[r * 32];
         }
         const double res = st.step(cf[r * 32], w, sea);
-        if (act) dst[k * nx] = static_cast<T>(res);
+        if (act) __stcs(dst + k * nx, static_cast<T>(res));
         if (sea && !mw.bit_next(k)) {  // segment end: raw closure input
           if (act) RAW[sA] = raw_state(st);
           ++sA;
@@ -239,11 +249,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         mw.at(W, k, a.words, true);
         const int sea = mw.bit(k);
         const Coef3 c = cf[r * 32];
-        if (sea && !nxt) st.enter(pf_take<TR>(pf, a.segs, RAW, CLline, nx, ny, G), c);
+        if (sea && !nxt) st.enter(eq.take(RAW), c);
         double o = st.step(c, static_cast<double>(fld[r * 32]));
         if (!TR && need_idc) o *= id[r * 32];
         if (POST) o *= __ldg(POST + k * nx);
-        if (act) dst[k * nx] = static_cast<T>(sea ? o : 0.0);
+        if (act) __stcs(dst + k * nx, static_cast<T>(sea ? o : 0.0));
         nxt = sea;
       }
     }
@@ -306,6 +316,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 
   if (warp == NW) {  // producer
     if (lane == 0) {
+      const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
       tma_prefetch_desc(&tm_in);
       tma_prefetch_desc(&tm_coef);
       const uint32_t total = static_cast<uint32_t>(L::field + L::coef + (need_idc ? L::idc : 0));
@@ -316,10 +327,12 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         const int k0 = static_cast<int>(k0_of(i));
         unsigned char* base = smem + s * L::bytes;
         mbar_arrive_expect_tx(&full[s], total);
-        tma_load_3d(base, &tm_in, k0, static_cast<int>(iy), static_cast<int>(p0), &full[s]);
-        tma_load_2d(base + L::field, &tm_coef, 4 * k0, static_cast<int>(iy), &full[s]);
+        tma_load_3d(base, &tm_in, k0, static_cast<int>(iy), static_cast<int>(p0), &full[s],
+                    pol_stream);
+        tma_load_2d(base + L::field, &tm_coef, 4 * k0, static_cast<int>(iy), &full[s], pol_keep);
         if (need_idc)
-          tma_load_2d(base + L::field + L::coef, &tm_idc, k0, static_cast<int>(iy), &full[s]);
+          tma_load_2d(base + L::field + L::coef, &tm_idc, k0, static_cast<int>(iy), &full[s],
+                      pol_keep);
       }
     }
     return;
@@ -335,15 +348,13 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + iy * n : nullptr;
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * ny + iy], s1 = a.seg_off[lev * ny + iy + 1];
-  const int G = a.ghost[lev];
-  const double* CLline = a.clos + ((int64_t)(a.cls[lev] * 2 + 0) * nh + iy * n) * 18;
   MaskWin mw;
   typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
                             typename std::conditional<TR, AdjA, FwdA>::type>::type st;
-  SegPrefetch pf;
+  EntryQ eq;
   int64_t sA = s0;
   int nxt = 0;
-  if constexpr (PD) pf_init<TR>(pf, s0, s1, a.segs, RAW, CLline, 1, n, G);
+  if constexpr (PD) eq.init(RAW, s0, s1);
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
@@ -398,7 +409,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
           mw.at(W, k, a.words, true);
           const int sea = mw.bit(k);
           const Coef3 c = cf[u];
-          if (sea && !nxt) st.enter(pf_take<TR>(pf, a.segs, RAW, CLline, 1, n, G), c);
+          if (sea && !nxt) st.enter(eq.take(RAW), c);
           double o = st.step(c, v[u]);
           if (!TR && need_idc) o *= id[u];
           if (POST) o *= __ldg(POST + k);
@@ -422,7 +433,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     fence_proxy_async_smem();
     asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NW) : "memory");
     if (threadIdx.x == 0) {
-      tma_store_3d(&tm_out, static_cast<int>(k0), static_cast<int>(iy), static_cast<int>(p0), base);
+      tma_store_3d(&tm_out, static_cast<int>(k0), static_cast<int>(iy), static_cast<int>(p0), base,
+                   l2_evict_first());
       bulk_commit();
       // the stage is free once the store has read it (the previous stage's
       // store is older; wait for it before releasing that stage)
@@ -511,24 +523,30 @@ void launch_xtma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
 
 template <typename T>
 int launch_tma_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+  const int64_t chains = a.nvar * a.nlev * (a.dir == 0 ? a.ny : a.nx);
+  const int64_t cblocks = (chains + 127) / 128;
   if (a.dir == 1) {
     if (a.transpose) {
       launch_ytma<T, true, false>(in, out, a, st);
+      k_close<1, true><<<cblocks, 128, 0, st>>>(a);
       launch_ytma<T, true, true>(out, out, a, st);
     } else {
       launch_ytma<T, false, false>(in, out, a, st);
+      k_close<1, false><<<cblocks, 128, 0, st>>>(a);
       launch_ytma<T, false, true>(out, out, a, st);
     }
   } else {
     if (a.transpose) {
       launch_xtma<T, true, false>(in, out, a, st);
+      k_close<0, true><<<cblocks, 128, 0, st>>>(a);
       launch_xtma<T, true, true>(out, out, a, st);
     } else {
       launch_xtma<T, false, false>(in, out, a, st);
+      k_close<0, false><<<cblocks, 128, 0, st>>>(a);
       launch_xtma<T, false, true>(out, out, a, st);
     }
   }
-  return 2;
+  return 3;
 }
 
 }  // namespace rgfb
