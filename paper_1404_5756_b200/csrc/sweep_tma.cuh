@@ -105,26 +105,65 @@ __device__ __forceinline__ double4 raw_state(const AdjA& s) {
   return make_double4(fma(s.x1, s.u1, s.y33 + s.y22), s.y32 + s.y21, s.y31, 0.0);
 }
 
-// mask word window: bits of positions [64w, 64w+64) and the next word
-struct MaskWin {
-  int64_t w = -2;
-  uint64_t cur = 0, nxt = 0;
-  __device__ __forceinline__ void at(const uint64_t* W, int64_t k, int64_t words, bool desc) {
-    const int64_t wi = k >> 6;
-    if (wi == w) return;
-    const int64_t wn = desc ? wi - 1 : wi + 1;
-    if ((desc ? wi == w - 1 : wi == w + 1)) {
-      cur = nxt;
-    } else {
-      cur = ldw(W, wi);
-    }
-    nxt = (wn >= 0 && wn < words) ? ldw(W, wn) : 0ull;
-    w = wi;
+// Lean pass-A states: no per-element land handling. The state is reset at
+// each segment start (the reference's zero initial state); values computed on
+// land are never stored as results (pass D masks land to exactly 0) and never
+// reach a segment because the next segment starts with a reset.
+struct FwdA2 {
+  double p1 = 0.0, p2 = 0.0, p3 = 0.0;
+  __device__ __forceinline__ void reset() { p1 = p2 = p3 = 0.0; }
+  __device__ __forceinline__ double step(const Coef3& c, double s) {
+    const double t = fma(c.a1, p1, fma(c.a2, p2, fma(c.a3, p3, c.b * s)));
+    p3 = p2;
+    p2 = p1;
+    p1 = t;
+    return t;
   }
-  __device__ __forceinline__ int bit(int64_t k) const { return int((cur >> (k & 63)) & 1ull); }
-  // sea(k+1) for the ascending pass
-  __device__ __forceinline__ int bit_next(int64_t k) const {
-    return (k & 63) == 63 ? int(nxt & 1ull) : int((cur >> ((k & 63) + 1)) & 1ull);
+  __device__ __forceinline__ double4 raw() const { return make_double4(p1, p2, p3, 0.0); }
+};
+struct AdjA2 {
+  double u1 = 0.0, x1 = 0.0, y21 = 0.0, y22 = 0.0, y31 = 0.0, y32 = 0.0, y33 = 0.0;
+  __device__ __forceinline__ void reset() { u1 = x1 = y21 = y22 = y31 = y32 = y33 = 0.0; }
+  __device__ __forceinline__ double step(const Coef3& c, double w) {
+    const double u = fma(x1, u1, (w + y33) + y22);
+    y33 = y32;
+    y32 = y31;
+    y31 = c.a3 * u;
+    y22 = y21;
+    y21 = c.a2 * u;
+    x1 = c.a1;
+    u1 = u;
+    return u;
+  }
+  // pending causal-transpose contributions into the first three ghosts
+  __device__ __forceinline__ double4 raw() const {
+    return make_double4(fma(x1, u1, y33 + y22), y32 + y21, y31, 0.0);
+  }
+};
+
+// One-word-lookahead mask window, advanced once per stage. Stages never
+// straddle a 64-bit word (U divides 64 and stages start at multiples of U).
+struct StageBits {
+  int64_t wi = -1;
+  uint64_t cur = 0, nxt = 0;
+  __device__ __forceinline__ void seek(const uint64_t* W, int64_t k, int64_t words, bool desc) {
+    const int64_t w = k >> 6;
+    if (w == wi) return;
+    cur = (wi >= 0 && w == (desc ? wi - 1 : wi + 1)) ? nxt : ldw(W, w);
+    const int64_t wn = desc ? w - 1 : w + 1;
+    nxt = (wn >= 0 && wn < words) ? ldw(W, wn) : 0ull;
+    wi = w;
+  }
+  template <int U>
+  __device__ __forceinline__ uint32_t stage(int64_t k0) const {
+    return static_cast<uint32_t>((cur >> (k0 & 63)) & ((1ull << U) - 1ull));
+  }
+  // sea(k0 + U) for an ascending pass (first bit of the following stage)
+  template <int U>
+  __device__ __forceinline__ uint32_t after(int64_t k0) const {
+    const int64_t kb = k0 + U;
+    return (kb & 63) == 0 ? static_cast<uint32_t>(nxt & 1ull)
+                          : static_cast<uint32_t>((cur >> (kb & 63)) & 1ull);
   }
 };
 
@@ -168,7 +207,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     mbar_fence_init();
   }
   __syncthreads();
-  auto lo_of = [&](int64_t i) -> int64_t { return PD ? ny - (i + 1) * U : i * U; };
+  auto lo_of = [&](int64_t i) -> int64_t { return (PD ? nst - 1 - i : i) * U; };
 
   if (warp == NW) {  // producer
     if (lane == 0) {
@@ -207,55 +246,58 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + ix : nullptr;
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * nx + ix], s1 = a.seg_off[lev * nx + ix + 1];
-  MaskWin mw;
-
+  StageBits sbw;
   typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
-                            typename std::conditional<TR, AdjA, FwdA>::type>::type st;
+                            typename std::conditional<TR, AdjA2, FwdA2>::type>::type st;
   EntryQ eq;
-  int64_t sA = s0;  // pass A: next segment index to be closed
-  int nxt = 0;
+  int64_t sA = s0;      // pass A: next segment index to be closed
+  uint32_t carry = 0;   // A: sea(lo-1); D: sea(lo+U)
   if constexpr (PD) eq.init(RAW, s0, s1);
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
-    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
     const int64_t lo = lo_of(i);
+    sbw.seek(W, lo, a.words, PD);
+    const uint32_t sb = sbw.stage<U>(lo);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
     const unsigned char* base = smem + s * L::bytes;
     const T* fld = reinterpret_cast<const T*>(base) + warp * U * 32 + lane;
     const Coef3* cf = reinterpret_cast<const Coef3*>(base + L::field) + lane;
     const double* id = reinterpret_cast<const double*>(base + L::field + L::coef) + lane;
+    T* drow = dst + lo * nx;
+    const bool full_stage = lo + U <= ny;
     if constexpr (!PD) {
-      const int nr = static_cast<int>(ny - lo < U ? ny - lo : U);
-      for (int r = 0; r < nr; ++r) {
-        const int64_t k = lo + r;
-        mw.at(W, k, a.words, false);
-        const int sea = mw.bit(k);
+      const uint32_t starts = sb & ~((sb << 1) | carry);
+      const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(lo) << (U - 1)));
+#pragma unroll 2
+      for (int r = 0; r < U; ++r) {
+        if ((starts >> r) & 1u) st.reset();
         double w = static_cast<double>(fld[r * 32]);
         if (TR) {
-          if (PRE) w *= __ldg(PRE + k * nx);
+          if (PRE) w *= __ldg(PRE + (lo + r) * nx);
           if (need_idc) w *= id[r * 32];
         }
-        const double res = st.step(cf[r * 32], w, sea);
-        if (act) __stcs(dst + k * nx, static_cast<T>(res));
-        if (sea && !mw.bit_next(k)) {  // segment end: raw closure input
-          if (act) RAW[sA] = raw_state(st);
+        const double res = st.step(cf[r * 32], w);
+        if (act && (full_stage || lo + r < ny)) __stcs(drow + r * nx, static_cast<T>(res));
+        if ((ends >> r) & 1u) {
+          if (act) RAW[sA] = st.raw();
           ++sA;
         }
       }
+      carry = (sb >> (U - 1)) & 1u;
     } else {
-      const int rmin = static_cast<int>(lo < 0 ? -lo : 0);
-      for (int r = U - 1; r >= rmin; --r) {
-        const int64_t k = lo + r;
-        mw.at(W, k, a.words, true);
-        const int sea = mw.bit(k);
+      const uint32_t events = sb & ~((sb >> 1) | (carry << (U - 1)));
+#pragma unroll 2
+      for (int r = U - 1; r >= 0; --r) {
         const Coef3 c = cf[r * 32];
-        if (sea && !nxt) st.enter(eq.take(RAW), c);
+        if ((events >> r) & 1u) st.enter(eq.take(RAW), c);
         double o = st.step(c, static_cast<double>(fld[r * 32]));
         if (!TR && need_idc) o *= id[r * 32];
-        if (POST) o *= __ldg(POST + k * nx);
-        if (act) __stcs(dst + k * nx, static_cast<T>(sea ? o : 0.0));
-        nxt = sea;
+        if (POST) o *= __ldg(POST + (lo + r) * nx);
+        if (act && (full_stage || lo + r < ny))
+          __stcs(drow + r * nx, static_cast<T>(((sb >> r) & 1u) ? o : 0.0));
       }
+      carry = sb & 1u;
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -348,19 +390,20 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + iy * n : nullptr;
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * ny + iy], s1 = a.seg_off[lev * ny + iy + 1];
-  MaskWin mw;
+  StageBits sbw;
   typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
-                            typename std::conditional<TR, AdjA, FwdA>::type>::type st;
+                            typename std::conditional<TR, AdjA2, FwdA2>::type>::type st;
   EntryQ eq;
   int64_t sA = s0;
-  int nxt = 0;
+  uint32_t carry = 0;  // A: sea(k0-1); D: sea(k0+U)
   if constexpr (PD) eq.init(RAW, s0, s1);
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
-    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
     const int64_t k0 = k0_of(i);
-    const int nk = static_cast<int>(n - k0 < U ? n - k0 : U);
+    sbw.seek(W, k0, a.words, PD);
+    const uint32_t sb = sbw.stage<U>(k0);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
     unsigned char* base = smem + s * L::bytes;
     const Coef3* cf = reinterpret_cast<const Coef3*>(base + L::field);
     const double* id = reinterpret_cast<const double*>(base + L::field + L::coef);
@@ -383,40 +426,35 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       }
     }
     if constexpr (!PD) {
+      const uint32_t starts = sb & ~((sb << 1) | carry);
+      const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(k0) << (U - 1)));
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        if (u < nk) {
-          const int64_t k = k0 + u;
-          mw.at(W, k, a.words, false);
-          const int sea = mw.bit(k);
-          double w = v[u];
-          if (TR) {
-            if (PRE) w *= __ldg(PRE + k);
-            if (need_idc) w *= id[u];
-          }
-          v[u] = st.step(cf[u], w, sea);
-          if (sea && !mw.bit_next(k)) {
-            if (act) RAW[sA] = raw_state(st);
-            ++sA;
-          }
+        if ((starts >> u) & 1u) st.reset();
+        double w = v[u];
+        if (TR) {
+          if (PRE) w *= __ldg(PRE + k0 + u);
+          if (need_idc) w *= id[u];
+        }
+        v[u] = st.step(cf[u], w);
+        if ((ends >> u) & 1u) {
+          if (act) RAW[sA] = st.raw();
+          ++sA;
         }
       }
+      carry = (sb >> (U - 1)) & 1u;
     } else {
+      const uint32_t events = sb & ~((sb >> 1) | (carry << (U - 1)));
 #pragma unroll
       for (int u = U - 1; u >= 0; --u) {
-        if (u < nk) {
-          const int64_t k = k0 + u;
-          mw.at(W, k, a.words, true);
-          const int sea = mw.bit(k);
-          const Coef3 c = cf[u];
-          if (sea && !nxt) st.enter(eq.take(RAW), c);
-          double o = st.step(c, v[u]);
-          if (!TR && need_idc) o *= id[u];
-          if (POST) o *= __ldg(POST + k);
-          v[u] = sea ? o : 0.0;
-          nxt = sea;
-        }
+        const Coef3 c = cf[u];
+        if ((events >> u) & 1u) st.enter(eq.take(RAW), c);
+        double o = st.step(c, v[u]);
+        if (!TR && need_idc) o *= id[u];
+        if (POST) o *= __ldg(POST + k0 + u);
+        v[u] = ((sb >> u) & 1u) ? o : 0.0;
       }
+      carry = sb & 1u;
     }
 #pragma unroll
     for (int q = 0; q < U / EPC; ++q) {
