@@ -181,9 +181,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     k_ytma(T* __restrict__ out, StreamArgs a, const __grid_constant__ CUtensorMap tm_field,
            const __grid_constant__ CUtensorMap tm_coef, const __grid_constant__ CUtensorMap tm_idc) {
   using L = YT<T, NW, U>;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1024 B alignment by pointer arithmetic (keeps the shared address space)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::bytes);
   uint64_t* empty = full + S;
 
@@ -269,7 +269,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     if constexpr (!PD) {
       const uint32_t starts = sb & ~((sb << 1) | carry);
       const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(lo) << (U - 1)));
-#pragma unroll 2
+#pragma unroll 1
       for (int r = 0; r < U; ++r) {
         if ((starts >> r) & 1u) st.reset();
         double w = static_cast<double>(fld[r * 32]);
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       carry = (sb >> (U - 1)) & 1u;
     } else {
       const uint32_t events = sb & ~((sb >> 1) | (carry << (U - 1)));
-#pragma unroll 2
+#pragma unroll 1
       for (int r = U - 1; r >= 0; --r) {
         const Coef3 c = cf[r * 32];
         if ((events >> r) & 1u) st.enter(eq.take(RAW), c);
@@ -329,9 +329,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
            const __grid_constant__ CUtensorMap tm_idc) {
   using L = XT<T, NW>;
   constexpr int U = L::U;
-  extern __shared__ unsigned char smem_raw[];
-  unsigned char* smem = reinterpret_cast<unsigned char*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  // 1024 B alignment by pointer arithmetic (keeps the shared address space)
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::bytes);
   uint64_t* empty = full + S;
 
@@ -407,65 +407,88 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     unsigned char* base = smem + s * L::bytes;
     const Coef3* cf = reinterpret_cast<const Coef3*>(base + L::field);
     const double* id = reinterpret_cast<const double*>(base + L::field + L::coef);
-    // this lane's U elements (128 B) through the swizzle, 16 B at a time
+    // this lane's U elements (128 B), 16 B chunk at a time through the swizzle
     constexpr int EPC = 16 / int(sizeof(T));  // elements per 16 B chunk
-    double v[U];
-#pragma unroll
-    for (int q = 0; q < U / EPC; ++q) {
-      const uint32_t off = swz128(pr, q * 16);
-      if constexpr (sizeof(T) == 8) {
-        const double2 t = *reinterpret_cast<const double2*>(base + off);
-        v[2 * q] = t.x;
-        v[2 * q + 1] = t.y;
-      } else {
-        const float4 t = *reinterpret_cast<const float4*>(base + off);
-        v[4 * q] = t.x;
-        v[4 * q + 1] = t.y;
-        v[4 * q + 2] = t.z;
-        v[4 * q + 3] = t.w;
-      }
-    }
+    unsigned char* rowp = base + pr * 128;
+    const int sw = pr & 7;
     if constexpr (!PD) {
       const uint32_t starts = sb & ~((sb << 1) | carry);
       const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(k0) << (U - 1)));
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        if ((starts >> u) & 1u) st.reset();
-        double w = v[u];
-        if (TR) {
-          if (PRE) w *= __ldg(PRE + k0 + u);
-          if (need_idc) w *= id[u];
+#pragma unroll 1
+      for (int q = 0; q < U / EPC; ++q) {
+        void* cp = rowp + ((q ^ sw) << 4);
+        double v[EPC];
+        if constexpr (sizeof(T) == 8) {
+          const double2 t = *reinterpret_cast<const double2*>(cp);
+          v[0] = t.x;
+          v[1] = t.y;
+        } else {
+          const float4 t = *reinterpret_cast<const float4*>(cp);
+          v[0] = t.x;
+          v[1] = t.y;
+          v[2] = t.z;
+          v[3] = t.w;
         }
-        v[u] = st.step(cf[u], w);
-        if ((ends >> u) & 1u) {
-          if (act) RAW[sA] = st.raw();
-          ++sA;
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const int u = q * EPC + e;
+          if ((starts >> u) & 1u) st.reset();
+          double w = v[e];
+          if (TR) {
+            if (PRE) w *= __ldg(PRE + k0 + u);
+            if (need_idc) w *= id[u];
+          }
+          v[e] = st.step(cf[u], w);
+          if ((ends >> u) & 1u) {
+            if (act) RAW[sA] = st.raw();
+            ++sA;
+          }
+        }
+        if constexpr (sizeof(T) == 8) {
+          *reinterpret_cast<double2*>(cp) = make_double2(v[0], v[1]);
+        } else {
+          *reinterpret_cast<float4*>(cp) =
+              make_float4(static_cast<float>(v[0]), static_cast<float>(v[1]),
+                          static_cast<float>(v[2]), static_cast<float>(v[3]));
         }
       }
       carry = (sb >> (U - 1)) & 1u;
     } else {
       const uint32_t events = sb & ~((sb >> 1) | (carry << (U - 1)));
+#pragma unroll 1
+      for (int q = U / EPC - 1; q >= 0; --q) {
+        void* cp = rowp + ((q ^ sw) << 4);
+        double v[EPC];
+        if constexpr (sizeof(T) == 8) {
+          const double2 t = *reinterpret_cast<const double2*>(cp);
+          v[0] = t.x;
+          v[1] = t.y;
+        } else {
+          const float4 t = *reinterpret_cast<const float4*>(cp);
+          v[0] = t.x;
+          v[1] = t.y;
+          v[2] = t.z;
+          v[3] = t.w;
+        }
 #pragma unroll
-      for (int u = U - 1; u >= 0; --u) {
-        const Coef3 c = cf[u];
-        if ((events >> u) & 1u) st.enter(eq.take(RAW), c);
-        double o = st.step(c, v[u]);
-        if (!TR && need_idc) o *= id[u];
-        if (POST) o *= __ldg(POST + k0 + u);
-        v[u] = ((sb >> u) & 1u) ? o : 0.0;
+        for (int e = EPC - 1; e >= 0; --e) {
+          const int u = q * EPC + e;
+          const Coef3 c = cf[u];
+          if ((events >> u) & 1u) st.enter(eq.take(RAW), c);
+          double o = st.step(c, v[e]);
+          if (!TR && need_idc) o *= id[u];
+          if (POST) o *= __ldg(POST + k0 + u);
+          v[e] = ((sb >> u) & 1u) ? o : 0.0;
+        }
+        if constexpr (sizeof(T) == 8) {
+          *reinterpret_cast<double2*>(cp) = make_double2(v[0], v[1]);
+        } else {
+          *reinterpret_cast<float4*>(cp) =
+              make_float4(static_cast<float>(v[0]), static_cast<float>(v[1]),
+                          static_cast<float>(v[2]), static_cast<float>(v[3]));
+        }
       }
       carry = sb & 1u;
-    }
-#pragma unroll
-    for (int q = 0; q < U / EPC; ++q) {
-      const uint32_t off = swz128(pr, q * 16);
-      if constexpr (sizeof(T) == 8) {
-        *reinterpret_cast<double2*>(base + off) = make_double2(v[2 * q], v[2 * q + 1]);
-      } else {
-        *reinterpret_cast<float4*>(base + off) =
-            make_float4(static_cast<float>(v[4 * q]), static_cast<float>(v[4 * q + 1]),
-                        static_cast<float>(v[4 * q + 2]), static_cast<float>(v[4 * q + 3]));
-      }
     }
     // all consumers' results in smem -> one TMA store of the box
     fence_proxy_async_smem();
