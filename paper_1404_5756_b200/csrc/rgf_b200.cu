@@ -100,6 +100,7 @@ struct DirData {
   DevBuf<double> idc;
   DevBuf<int64_t> seg_off;  // nlev*lines + 1
   DevBuf<int2> segs;
+  DevBuf<int32_t> seg_line;  // per segment: lev*lines + line
   int64_t nsegs = 0;
   std::vector<char> uniform;        // per level
   std::vector<double> sigma_u;      // per level, uniform sigma value
@@ -168,6 +169,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.clos = op->clos.p;
     a.seg_off = d.seg_off.p;
     a.segs = d.segs.p;
+    a.seg_line = d.seg_line.p;
     a.nsegs = d.nsegs;
     op->entry.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs)));
     a.entry = op->entry.p;
@@ -281,8 +283,9 @@ void build_segments(rgf_op* op, const uint8_t* mask_d, int dir, DirData& d) {
   CUDA_OK(cudaMemcpy(&total, d.seg_off.p + lines, sizeof(int64_t), cudaMemcpyDeviceToHost));
   d.nsegs = total;
   d.segs.alloc(std::max<int64_t>(total, 1));
+  d.seg_line.alloc(std::max<int64_t>(total, 1));
   rgfb::k_seg_fill<<<grid_for(lines, 128), 128>>>(mask_d, dir, op->nx, op->ny, lines,
-                                                  d.seg_off.p, d.segs.p);
+                                                  d.seg_off.p, d.segs.p, d.seg_line.p);
   CUDA_OK(cudaGetLastError());
   CUDA_OK(cudaDeviceSynchronize());
 }
@@ -561,7 +564,8 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
                  op->bits[0].bytes() + op->bits[1].bytes() + op->clos.bytes() + op->cls_d.bytes() + op->entry.bytes() +
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})
-      b += d->c3.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes();
+      b += d->c3.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
+           d->seg_line.bytes();
     *out = b;
   });
 }

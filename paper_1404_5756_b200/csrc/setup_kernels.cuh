@@ -151,7 +151,8 @@ __global__ void k_seg_count(const uint8_t* mask, int dir, int64_t nx, int64_t ny
 }
 
 __global__ void k_seg_fill(const uint8_t* mask, int dir, int64_t nx, int64_t ny,
-                           int64_t nlines, const int64_t* offsets, int2* segs) {
+                           int64_t nlines, const int64_t* offsets, int2* segs,
+                           int32_t* seg_line) {
   const int64_t n = dir == 0 ? nx : ny;
   for (int64_t line = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; line < nlines;
        line += (int64_t)gridDim.x * blockDim.x) {
@@ -164,6 +165,7 @@ __global__ void k_seg_fill(const uint8_t* mask, int dir, int64_t nx, int64_t ny,
       }
       int64_t j = i;
       while (j + 1 < n && line_sea(mask, dir, nx, ny, line, j + 1)) ++j;
+      seg_line[o] = static_cast<int32_t>(line);  // (lev, line) of this segment
       segs[o++] = make_int2((int)i, (int)(j - i + 1));
       i = j + 1;
     }

@@ -63,37 +63,39 @@ struct EntryQ {
 };
 
 // Closure application between pass A and pass D: raw segment-end state ->
-// anti-causal entry state, in place, one thread per (line, plane) with
-// planes fastest so the planes of one line share the closure rows in L2.
+// anti-causal entry state, in place. One thread per segment (consecutive
+// threads, consecutive segments of one line): the closure row of the
+// segment's end point is loaded once and applied to every variable.
 template <int DIR, bool TR>
-__global__ void __launch_bounds__(128) k_close(StreamArgs a) {
+__global__ void __launch_bounds__(256) k_close(StreamArgs a) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= a.nsegs) return;
   const int64_t n = DIR == 0 ? a.nx : a.ny;
   const int64_t nlines = DIR == 0 ? a.ny : a.nx;
   const int64_t nh = a.nx * a.ny;
-  const int64_t stride = DIR == 0 ? 1 : a.nx;
-  const int64_t planes = a.nvar * a.nlev;
-  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (tid >= planes * nlines) return;
-  const int64_t line = tid / planes;
-  const int64_t p = tid - line * planes;
-  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
-  const int64_t hb = DIR == 0 ? line * a.nx : line;
+  const int64_t lg = __ldg(a.seg_line + s);
+  const int64_t lev = lg / nlines, line = lg - lev * nlines;
+  const int2 sg = __ldg(a.segs + s);
+  const int64_t j = sg.x + sg.y - 1;
   const int G = a.ghost[lev];
-  const double* CL = a.clos + ((int64_t)(a.cls[lev] * 2 + DIR) * nh + hb) * 18 + (TR ? 9 : 0);
-  const int64_t s0 = a.seg_off[lev * nlines + line], s1 = a.seg_off[lev * nlines + line + 1];
-  double4* E = a.entry + var * a.nsegs;
-  for (int64_t s = s0; s < s1; ++s) {
-    const int2 sg = __ldg(a.segs + s);
-    const int64_t j = sg.x + sg.y - 1;
+  double M[9];
+  const bool ghost = j < n - 1 && G > 0;
+  if (ghost) {
+    const int64_t h = DIR == 0 ? line * a.nx + j : j * a.nx + line;
+    const double* Mp = a.clos + ((int64_t)(a.cls[lev] * 2 + DIR) * nh + h) * 18 + (TR ? 9 : 0);
+#pragma unroll
+    for (int q = 0; q < 9; ++q) M[q] = __ldg(Mp + q);
+  }
+  for (int64_t v = 0; v < a.nvar; ++v) {
+    double4* E = a.entry + v * a.nsegs + s;
     double4 e = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (j < n - 1 && G > 0) {
-      const double4 r = E[s];
-      const double* M = CL + j * stride * 18;
-      e.x = fma(__ldg(M + 0), r.x, fma(__ldg(M + 1), r.y, __ldg(M + 2) * r.z));
-      e.y = fma(__ldg(M + 3), r.x, fma(__ldg(M + 4), r.y, __ldg(M + 5) * r.z));
-      e.z = fma(__ldg(M + 6), r.x, fma(__ldg(M + 7), r.y, __ldg(M + 8) * r.z));
+    if (ghost) {
+      const double4 r = *E;
+      e.x = fma(M[0], r.x, fma(M[1], r.y, M[2] * r.z));
+      e.y = fma(M[3], r.x, fma(M[4], r.y, M[5] * r.z));
+      e.z = fma(M[6], r.x, fma(M[7], r.y, M[8] * r.z));
     }
-    E[s] = e;
+    *E = e;
   }
 }
 
@@ -176,7 +178,7 @@ struct YT {
   static constexpr size_t bytes = field + coef + idc;
 };
 
-template <typename T, bool TR, bool PD, int NW, int U, int S>
+template <typename T, bool TR, bool PD, bool IDC, bool VAR, int NW, int U, int S>
 __global__ void __launch_bounds__(32 * (NW + 1), 1)
     k_ytma(T* __restrict__ out, StreamArgs a, const __grid_constant__ CUtensorMap tm_field,
            const __grid_constant__ CUtensorMap tm_coef, const __grid_constant__ CUtensorMap tm_idc) {
@@ -195,7 +197,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const int64_t ix0 = tile * 32;
   const int ncol = static_cast<int>(nx - ix0 < 32 ? nx - ix0 : 32);
   const int nwp = static_cast<int>(planes - p0 < NW ? planes - p0 : NW);
-  const bool need_idc = a.idc != nullptr && (PD ? !TR : TR);
+  constexpr bool need_idc = IDC;  // inv_dc table staged (fwd pass D / adjoint pass A)
   const int64_t nst = (ny + U - 1) / U;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -242,8 +244,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const int64_t ix = ix0 + (act ? lane : 0);
   T* dst = out + p * nh + ix;
   const uint64_t* W = a.bits + (lev * nx + ix) * a.words;
-  const double* PRE = (!PD && TR && a.pre_scale) ? a.pre_scale + lev * nh + ix : nullptr;
-  const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + ix : nullptr;
+  const double* PRE = (VAR && !PD && TR) ? a.pre_scale + lev * nh + ix : nullptr;
+  const double* POST = (VAR && PD) ? a.post_scale + lev * nh + ix : nullptr;
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * nx + ix], s1 = a.seg_off[lev * nx + ix + 1];
   StageBits sbw;
@@ -265,7 +267,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     const Coef3* cf = reinterpret_cast<const Coef3*>(base + L::field) + lane;
     const double* id = reinterpret_cast<const double*>(base + L::field + L::coef) + lane;
     T* drow = dst + lo * nx;
-    const bool full_stage = lo + U <= ny;
+    const int rvalid = act ? static_cast<int>(ny - lo < U ? ny - lo : U) : 0;
     if constexpr (!PD) {
       const uint32_t starts = sb & ~((sb << 1) | carry);
       const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(lo) << (U - 1)));
@@ -274,11 +276,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         if ((starts >> r) & 1u) st.reset();
         double w = static_cast<double>(fld[r * 32]);
         if (TR) {
-          if (PRE) w *= __ldg(PRE + (lo + r) * nx);
-          if (need_idc) w *= id[r * 32];
+          if constexpr (VAR) w *= __ldg(PRE + (lo + r) * nx);
+          if constexpr (IDC) w *= id[r * 32];
         }
         const double res = st.step(cf[r * 32], w);
-        if (act && (full_stage || lo + r < ny)) __stcs(drow + r * nx, static_cast<T>(res));
+        if (r < rvalid) __stcs(drow + r * static_cast<int>(nx), static_cast<T>(res));
         if ((ends >> r) & 1u) {
           if (act) RAW[sA] = st.raw();
           ++sA;
@@ -292,10 +294,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         const Coef3 c = cf[r * 32];
         if ((events >> r) & 1u) st.enter(eq.take(RAW), c);
         double o = st.step(c, static_cast<double>(fld[r * 32]));
-        if (!TR && need_idc) o *= id[r * 32];
-        if (POST) o *= __ldg(POST + (lo + r) * nx);
-        if (act && (full_stage || lo + r < ny))
-          __stcs(drow + r * nx, static_cast<T>(((sb >> r) & 1u) ? o : 0.0));
+        if constexpr (!TR && IDC) o *= id[r * 32];
+        if constexpr (VAR) o *= __ldg(POST + (lo + r) * nx);
+        if (r < rvalid)
+          __stcs(drow + r * static_cast<int>(nx), static_cast<T>(((sb >> r) & 1u) ? o : 0.0));
       }
       carry = sb & 1u;
     }
@@ -322,7 +324,7 @@ __device__ __forceinline__ uint32_t swz128(int r, uint32_t byte_in_row) {
   return static_cast<uint32_t>(r) * 128u + ((((byte_in_row >> 4) ^ (r & 7)) << 4) | (byte_in_row & 15u));
 }
 
-template <typename T, bool TR, bool PD, int NW, int S>
+template <typename T, bool TR, bool PD, bool IDC, bool VAR, int NW, int S>
 __global__ void __launch_bounds__(32 * (NW + 1), 1)
     k_xtma(T* __restrict__ out, StreamArgs a, const __grid_constant__ CUtensorMap tm_in,
            const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ CUtensorMap tm_coef,
@@ -342,7 +344,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const int64_t p0 = (blockIdx.x - iy * PB) * 32 * NW;
   const int npl = static_cast<int>(planes - p0 < 32 * NW ? planes - p0 : 32 * NW);
   const int nwp = (npl + 31) / 32;
-  const bool need_idc = a.idc != nullptr && (PD ? !TR : TR);
+  constexpr bool need_idc = IDC;  // inv_dc table staged (fwd pass D / adjoint pass A)
   const int64_t nst = (n + U - 1) / U;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -386,8 +388,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const int64_t p = p0 + (act ? pr : 0);
   const int64_t var = p / a.nlev, lev = p - var * a.nlev;
   const uint64_t* W = a.bits + (lev * ny + iy) * a.words;
-  const double* PRE = (!PD && TR && a.pre_scale) ? a.pre_scale + lev * nh + iy * n : nullptr;
-  const double* POST = (PD && a.post_scale) ? a.post_scale + lev * nh + iy * n : nullptr;
+  const double* PRE = (VAR && !PD && TR) ? a.pre_scale + lev * nh + iy * n : nullptr;
+  const double* POST = (VAR && PD) ? a.post_scale + lev * nh + iy * n : nullptr;
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * ny + iy], s1 = a.seg_off[lev * ny + iy + 1];
   StageBits sbw;
@@ -435,8 +437,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
           if ((starts >> u) & 1u) st.reset();
           double w = v[e];
           if (TR) {
-            if (PRE) w *= __ldg(PRE + k0 + u);
-            if (need_idc) w *= id[u];
+            if constexpr (VAR) w *= __ldg(PRE + k0 + u);
+            if constexpr (IDC) w *= id[u];
           }
           v[e] = st.step(cf[u], w);
           if ((ends >> u) & 1u) {
@@ -476,8 +478,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
           const Coef3 c = cf[u];
           if ((events >> u) & 1u) st.enter(eq.take(RAW), c);
           double o = st.step(c, v[e]);
-          if (!TR && need_idc) o *= id[u];
-          if (POST) o *= __ldg(POST + k0 + u);
+          if constexpr (!TR && IDC) o *= id[u];
+          if constexpr (VAR) o *= __ldg(POST + k0 + u);
           v[e] = ((sb >> u) & 1u) ? o : 0.0;
         }
         if constexpr (sizeof(T) == 8) {
@@ -515,14 +517,14 @@ inline bool tma_supported(const T* in, const T* out, int64_t nx) {
          reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
 }
 
-template <typename T, bool TR, bool PD>
-void launch_ytma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+template <typename T, bool TR, bool PD, bool IDC, bool VAR>
+void launch_ytma_k(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   constexpr int NW = kYtNW, U = kYtU, S = kYtS;
   const size_t smem = S * YT<T, NW, U>::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_ytma<T, TR, PD, NW, U, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    cudaFuncSetAttribute(k_ytma<T, TR, PD, IDC, VAR, NW, U, S>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
   const int64_t planes = a.nvar * a.nlev;
@@ -544,18 +546,18 @@ void launch_ytma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
                                            CU_TENSOR_MAP_SWIZZLE_NONE)
                                : tc;
   const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NW - 1) / NW);
-  k_ytma<T, TR, PD, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tf, tc, ti);
+  k_ytma<T, TR, PD, IDC, VAR, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tf, tc, ti);
 }
 
-template <typename T, bool TR, bool PD>
-void launch_xtma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+template <typename T, bool TR, bool PD, bool IDC, bool VAR>
+void launch_xtma_k(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   constexpr int NW = kXtNW, S = kXtS;
   using L = XT<T, NW>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_xtma<T, TR, PD, NW, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(smem));
+    cudaFuncSetAttribute(k_xtma<T, TR, PD, IDC, VAR, NW, S>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
   const int64_t planes = a.nvar * a.nlev;
@@ -563,9 +565,12 @@ void launch_xtma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
   const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
   const uint32_t fb[3] = {uint32_t(L::U), 1, uint32_t(32 * NW)};
+  // box rows are exactly one 128 B line: no L2 over-fetch
   const CUtensorMap tin = make_tmap(PD ? static_cast<const void*>(out) : in, tma_dtype<T>(), 3,
-                                    fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B);
-  const CUtensorMap tout = make_tmap(out, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B);
+                                    fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+  const CUtensorMap tout = make_tmap(out, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B,
+                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
   const uint64_t cd[2] = {uint64_t(4 * a.nx), uint64_t(a.ny)};
   const uint64_t cs[1] = {uint64_t(4 * a.nx) * 8};
   const uint32_t cb[2] = {uint32_t(4 * L::U), 1};
@@ -579,31 +584,57 @@ void launch_xtma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
                                : tc;
   const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
   const int64_t blocks = a.ny * PB;
-  k_xtma<T, TR, PD, NW, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tin, tout, tc, ti);
+  k_xtma<T, TR, PD, IDC, VAR, NW, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tin, tout, tc,
+                                                                          ti);
+}
+
+// runtime flags -> template flags
+template <typename T, bool TR, bool PD>
+void launch_ytma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+  const bool idc = a.idc != nullptr && (PD ? !TR : TR);
+  const bool var = PD ? a.post_scale != nullptr : (TR && a.pre_scale != nullptr);
+  if (idc) {
+    if (var) launch_ytma_k<T, TR, PD, true, true>(in, out, a, st);
+    else launch_ytma_k<T, TR, PD, true, false>(in, out, a, st);
+  } else {
+    if (var) launch_ytma_k<T, TR, PD, false, true>(in, out, a, st);
+    else launch_ytma_k<T, TR, PD, false, false>(in, out, a, st);
+  }
+}
+template <typename T, bool TR, bool PD>
+void launch_xtma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
+  const bool idc = a.idc != nullptr && (PD ? !TR : TR);
+  const bool var = PD ? a.post_scale != nullptr : (TR && a.pre_scale != nullptr);
+  if (idc) {
+    if (var) launch_xtma_k<T, TR, PD, true, true>(in, out, a, st);
+    else launch_xtma_k<T, TR, PD, true, false>(in, out, a, st);
+  } else {
+    if (var) launch_xtma_k<T, TR, PD, false, true>(in, out, a, st);
+    else launch_xtma_k<T, TR, PD, false, false>(in, out, a, st);
+  }
 }
 
 template <typename T>
 int launch_tma_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
-  const int64_t chains = a.nvar * a.nlev * (a.dir == 0 ? a.ny : a.nx);
-  const int64_t cblocks = (chains + 127) / 128;
+  const int64_t cblocks = (a.nsegs + 255) / 256;
   if (a.dir == 1) {
     if (a.transpose) {
       launch_ytma<T, true, false>(in, out, a, st);
-      k_close<1, true><<<cblocks, 128, 0, st>>>(a);
+      k_close<1, true><<<cblocks, 256, 0, st>>>(a);
       launch_ytma<T, true, true>(out, out, a, st);
     } else {
       launch_ytma<T, false, false>(in, out, a, st);
-      k_close<1, false><<<cblocks, 128, 0, st>>>(a);
+      k_close<1, false><<<cblocks, 256, 0, st>>>(a);
       launch_ytma<T, false, true>(out, out, a, st);
     }
   } else {
     if (a.transpose) {
       launch_xtma<T, true, false>(in, out, a, st);
-      k_close<0, true><<<cblocks, 128, 0, st>>>(a);
+      k_close<0, true><<<cblocks, 256, 0, st>>>(a);
       launch_xtma<T, true, true>(out, out, a, st);
     } else {
       launch_xtma<T, false, false>(in, out, a, st);
-      k_close<0, false><<<cblocks, 128, 0, st>>>(a);
+      k_close<0, false><<<cblocks, 256, 0, st>>>(a);
       launch_xtma<T, false, true>(out, out, a, st);
     }
   }

@@ -31,12 +31,12 @@ inline PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 // rank-r tiled map; dims/strides in elements/bytes, dim 0 contiguous.
 inline CUtensorMap make_tmap(const void* base, CUtensorMapDataType dt, int rank,
                              const uint64_t* dims, const uint64_t* strides_bytes,
-                             const uint32_t* box, CUtensorMapSwizzle sw) {
+                             const uint32_t* box, CUtensorMapSwizzle sw,
+                             CUtensorMapL2promotion l2 = CU_TENSOR_MAP_L2_PROMOTION_L2_256B) {
   CUtensorMap m;
   uint32_t es[5] = {1, 1, 1, 1, 1};
   const CUresult r = tma_encoder()(&m, dt, rank, const_cast<void*>(base), dims, strides_bytes,
-                                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw,
-                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, l2,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS)
     throw std::runtime_error("cuTensorMapEncodeTiled failed (" + std::to_string(int(r)) + ")");
