@@ -33,71 +33,88 @@
 namespace rgfb {
 
 // ---------------------------------------------------------------- helpers
-// Pass D consumes the entry states of its segments in reverse order; a
-// 3-deep register ring keeps the next three in flight so a short segment
-// never waits for its entry.
-struct EntryQ {
-  int64_t next, first;  // index of the next entry to fetch into the ring
-  double3 q0, q1, q2;
-  __device__ __forceinline__ double3 ld(const double4* E, int64_t i) const {
-    if (i < first) return make_double3(0.0, 0.0, 0.0);
-    const double2 a = *reinterpret_cast<const double2*>(E + i);
-    const double b = reinterpret_cast<const double*>(E + i)[2];
-    return make_double3(a.x, a.y, b);
-  }
-  __device__ __forceinline__ void init(const double4* E, int64_t s0, int64_t s1) {
-    first = s0;
-    q0 = ld(E, s1 - 1);
-    q1 = ld(E, s1 - 2);
-    q2 = ld(E, s1 - 3);
-    next = s1 - 4;
-  }
-  __device__ __forceinline__ double4 take(const double4* E) {
-    const double4 e = make_double4(q0.x, q0.y, q0.z, 0.0);
-    q0 = q1;
-    q1 = q2;
-    q2 = ld(E, next);
-    --next;
-    return e;
-  }
-};
-
-// Closure application between pass A and pass D: raw segment-end state ->
-// anti-causal entry state, in place. One thread per segment (consecutive
-// threads, consecutive segments of one line): the closure row of the
-// segment's end point is loaded once and applied to every variable.
-template <int DIR, bool TR>
-__global__ void __launch_bounds__(256) k_close(StreamArgs a) {
+// Closure application between pass A and pass D. For every segment (one
+// thread per segment, all variables) the right-ghost closure turns the raw
+// causal state at the segment end j into the anti-causal entry
+// e = (q_{j+1}, q_{j+2}, q_{j+3}), and the entry's contributions are folded
+// into the stored pass-A terms at j, j-1, j-2 (inside the segment):
+//   forward  (w = beta p):  w_j += a1_j e1 + a2_j e2 + a3_j e3,
+//                           w_{j-1} += a2_{j-1} e1 + a3_{j-1} e2,
+//                           w_{j-2} += a3_{j-2} e1          (rf3.hpp:255-261)
+//   adjoint  (v = beta u):  same pattern with the ghost coefficients c_j
+//                           (sources beyond j; rf3.hpp:264-274 gather form).
+// Pass D then starts every segment from a zero state, exactly as the
+// reference's startup rows do at an extended segment's far end.
+template <typename T, int DIR, bool TR>
+__global__ void __launch_bounds__(256) k_close(T* __restrict__ z, StreamArgs a) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= a.nsegs) return;
   const int64_t n = DIR == 0 ? a.nx : a.ny;
   const int64_t nlines = DIR == 0 ? a.ny : a.nx;
   const int64_t nh = a.nx * a.ny;
+  const int64_t stride = DIR == 0 ? 1 : a.nx;
   const int64_t lg = __ldg(a.seg_line + s);
   const int64_t lev = lg / nlines, line = lg - lev * nlines;
   const int2 sg = __ldg(a.segs + s);
   const int64_t j = sg.x + sg.y - 1;
   const int G = a.ghost[lev];
+  if (!(j < n - 1 && G > 0)) return;  // no right ghosts: zero entry
+  const int64_t h = DIR == 0 ? line * a.nx + j : j * a.nx + line;
+  const double* Mp = a.clos + ((int64_t)(a.cls[lev] * 2 + DIR) * nh + h) * 18 + (TR ? 9 : 0);
   double M[9];
-  const bool ghost = j < n - 1 && G > 0;
-  if (ghost) {
-    const int64_t h = DIR == 0 ? line * a.nx + j : j * a.nx + line;
-    const double* Mp = a.clos + ((int64_t)(a.cls[lev] * 2 + DIR) * nh + h) * 18 + (TR ? 9 : 0);
 #pragma unroll
-    for (int q = 0; q < 9; ++q) M[q] = __ldg(Mp + q);
+  for (int q = 0; q < 9; ++q) M[q] = __ldg(Mp + q);
+  const Coef3 cj = ldc(a.c3 + h);
+  Coef3 c1 = cj, c2 = cj;  // coefficients feeding w_{j-1}, w_{j-2}
+  if (!TR) {
+    if (sg.y >= 2) c1 = ldc(a.c3 + h - stride);
+    if (sg.y >= 3) c2 = ldc(a.c3 + h - 2 * stride);
   }
   for (int64_t v = 0; v < a.nvar; ++v) {
-    double4* E = a.entry + v * a.nsegs + s;
-    double4 e = make_double4(0.0, 0.0, 0.0, 0.0);
-    if (ghost) {
-      const double4 r = *E;
-      e.x = fma(M[0], r.x, fma(M[1], r.y, M[2] * r.z));
-      e.y = fma(M[3], r.x, fma(M[4], r.y, M[5] * r.z));
-      e.z = fma(M[6], r.x, fma(M[7], r.y, M[8] * r.z));
-    }
-    *E = e;
+    const double4 r = a.entry[v * a.nsegs + s];
+    const double e1 = fma(M[0], r.x, fma(M[1], r.y, M[2] * r.z));
+    const double e2 = fma(M[3], r.x, fma(M[4], r.y, M[5] * r.z));
+    const double e3 = fma(M[6], r.x, fma(M[7], r.y, M[8] * r.z));
+    T* zl = z + ((v * a.nlev + lev) * nh + h);
+    *zl = static_cast<T>(static_cast<double>(*zl) +
+                         fma(cj.a1, e1, fma(cj.a2, e2, cj.a3 * e3)));
+    if (sg.y >= 2)
+      zl[-stride] = static_cast<T>(static_cast<double>(zl[-stride]) + fma(c1.a2, e1, c1.a3 * e2));
+    if (sg.y >= 3)
+      zl[-2 * stride] = static_cast<T>(static_cast<double>(zl[-2 * stride]) + c2.a3 * e1);
   }
 }
+
+// Lean pass-D states: the entry is already folded into the stored terms, so
+// a segment end is a plain reset.
+struct FwdD2 {
+  double q1 = 0.0, q2 = 0.0, q3 = 0.0;
+  __device__ __forceinline__ void reset() { q1 = q2 = q3 = 0.0; }
+  // w = beta p (+ folded entry)
+  __device__ __forceinline__ double step(const Coef3& c, double w) {
+    const double q = fma(c.a1, q1, fma(c.a2, q2, fma(c.a3, q3, w)));
+    q3 = q2;
+    q2 = q1;
+    q1 = q;
+    return q;
+  }
+};
+struct AdjD2 {
+  double U1 = 0.0, X1 = 0.0, Y21 = 0.0, Y22 = 0.0, Y31 = 0.0, Y32 = 0.0, Y33 = 0.0;
+  __device__ __forceinline__ void reset() { U1 = Y21 = Y22 = Y31 = Y32 = Y33 = 0.0; }
+  // v = beta u (+ folded entry); returns beta u'
+  __device__ __forceinline__ double step(const Coef3& c, double v) {
+    const double u = fma(X1, U1, (v + Y33) + Y22);
+    Y33 = Y32;
+    Y32 = Y31;
+    Y31 = c.a3 * u;
+    Y22 = Y21;
+    Y21 = c.a2 * u;
+    X1 = c.a1;
+    U1 = u;
+    return c.b * u;
+  }
+};
 
 // raw state written by pass A at a segment end
 __device__ __forceinline__ double4 raw_state(const FwdA& s) {
@@ -249,12 +266,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * nx + ix], s1 = a.seg_off[lev * nx + ix + 1];
   StageBits sbw;
-  typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
+  typename std::conditional<PD, typename std::conditional<TR, AdjD2, FwdD2>::type,
                             typename std::conditional<TR, AdjA2, FwdA2>::type>::type st;
-  EntryQ eq;
   int64_t sA = s0;      // pass A: next segment index to be closed
   uint32_t carry = 0;   // A: sea(lo-1); D: sea(lo+U)
-  if constexpr (PD) eq.init(RAW, s0, s1);
+  (void)s1;
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
@@ -271,7 +287,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     if constexpr (!PD) {
       const uint32_t starts = sb & ~((sb << 1) | carry);
       const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(lo) << (U - 1)));
-#pragma unroll 1
+#pragma unroll
       for (int r = 0; r < U; ++r) {
         if ((starts >> r) & 1u) st.reset();
         double w = static_cast<double>(fld[r * 32]);
@@ -279,7 +295,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
           if constexpr (VAR) w *= __ldg(PRE + (lo + r) * nx);
           if constexpr (IDC) w *= id[r * 32];
         }
-        const double res = st.step(cf[r * 32], w);
+        const Coef3 c = cf[r * 32];
+        const double res = c.b * st.step(c, w);  // stored term beta*p / beta*u
         if (r < rvalid) __stcs(drow + r * static_cast<int>(nx), static_cast<T>(res));
         if ((ends >> r) & 1u) {
           if (act) RAW[sA] = st.raw();
@@ -289,10 +306,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       carry = (sb >> (U - 1)) & 1u;
     } else {
       const uint32_t events = sb & ~((sb >> 1) | (carry << (U - 1)));
-#pragma unroll 1
+#pragma unroll
       for (int r = U - 1; r >= 0; --r) {
         const Coef3 c = cf[r * 32];
-        if ((events >> r) & 1u) st.enter(eq.take(RAW), c);
+        if ((events >> r) & 1u) st.reset();
         double o = st.step(c, static_cast<double>(fld[r * 32]));
         if constexpr (!TR && IDC) o *= id[r * 32];
         if constexpr (VAR) o *= __ldg(POST + (lo + r) * nx);
@@ -393,12 +410,11 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   double4* RAW = a.entry + var * a.nsegs;
   const int64_t s0 = a.seg_off[lev * ny + iy], s1 = a.seg_off[lev * ny + iy + 1];
   StageBits sbw;
-  typename std::conditional<PD, typename std::conditional<TR, AdjD, FwdD>::type,
+  typename std::conditional<PD, typename std::conditional<TR, AdjD2, FwdD2>::type,
                             typename std::conditional<TR, AdjA2, FwdA2>::type>::type st;
-  EntryQ eq;
   int64_t sA = s0;
   uint32_t carry = 0;  // A: sea(k0-1); D: sea(k0+U)
-  if constexpr (PD) eq.init(RAW, s0, s1);
+  (void)s1;
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
@@ -440,7 +456,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
             if constexpr (VAR) w *= __ldg(PRE + k0 + u);
             if constexpr (IDC) w *= id[u];
           }
-          v[e] = st.step(cf[u], w);
+          const Coef3 c = cf[u];
+          v[e] = c.b * st.step(c, w);  // stored term beta*p / beta*u
           if ((ends >> u) & 1u) {
             if (act) RAW[sA] = st.raw();
             ++sA;
@@ -476,7 +493,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         for (int e = EPC - 1; e >= 0; --e) {
           const int u = q * EPC + e;
           const Coef3 c = cf[u];
-          if ((events >> u) & 1u) st.enter(eq.take(RAW), c);
+          if ((events >> u) & 1u) st.reset();
           double o = st.step(c, v[e]);
           if constexpr (!TR && IDC) o *= id[u];
           if constexpr (VAR) o *= __ldg(POST + k0 + u);
@@ -620,21 +637,21 @@ int launch_tma_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) 
   if (a.dir == 1) {
     if (a.transpose) {
       launch_ytma<T, true, false>(in, out, a, st);
-      k_close<1, true><<<cblocks, 256, 0, st>>>(a);
+      k_close<T, 1, true><<<cblocks, 256, 0, st>>>(out, a);
       launch_ytma<T, true, true>(out, out, a, st);
     } else {
       launch_ytma<T, false, false>(in, out, a, st);
-      k_close<1, false><<<cblocks, 256, 0, st>>>(a);
+      k_close<T, 1, false><<<cblocks, 256, 0, st>>>(out, a);
       launch_ytma<T, false, true>(out, out, a, st);
     }
   } else {
     if (a.transpose) {
       launch_xtma<T, true, false>(in, out, a, st);
-      k_close<0, true><<<cblocks, 256, 0, st>>>(a);
+      k_close<T, 0, true><<<cblocks, 256, 0, st>>>(out, a);
       launch_xtma<T, true, true>(out, out, a, st);
     } else {
       launch_xtma<T, false, false>(in, out, a, st);
-      k_close<0, false><<<cblocks, 256, 0, st>>>(a);
+      k_close<T, 0, false><<<cblocks, 256, 0, st>>>(out, a);
       launch_xtma<T, false, true>(out, out, a, st);
     }
   }
