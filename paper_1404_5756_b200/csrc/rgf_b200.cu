@@ -5,6 +5,7 @@
 // segmentation kernels; the seven apply_* methods (covariance.cpp:362-398)
 // become sequences of sweep kernels on one CUDA stream. No CPU arithmetic
 // touches field values.
+#include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
@@ -101,6 +102,7 @@ struct DirData {
   DevBuf<int64_t> seg_off;  // nlev*lines + 1
   DevBuf<int2> segs;
   DevBuf<int32_t> seg_line;  // per segment: lev*lines + line
+  DevBuf<int64_t> close_order;  // segments sorted by (line, end, level)
   int64_t nsegs = 0;
   std::vector<char> uniform;        // per level
   std::vector<double> sigma_u;      // per level, uniform sigma value
@@ -170,6 +172,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.seg_off = d.seg_off.p;
     a.segs = d.segs.p;
     a.seg_line = d.seg_line.p;
+    a.close_order = d.close_order.p;
     a.nsegs = d.nsegs;
     op->entry.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs)));
     a.entry = op->entry.p;
@@ -287,6 +290,26 @@ void build_segments(rgf_op* op, const uint8_t* mask_d, int dir, DirData& d) {
   rgfb::k_seg_fill<<<grid_for(lines, 128), 128>>>(mask_d, dir, op->nx, op->ny, lines,
                                                   d.seg_off.p, d.segs.p, d.seg_line.p);
   CUDA_OK(cudaGetLastError());
+  if (total > 0) {  // closure-pass order: (line, end, level)
+    const int64_t nl = dir == 0 ? op->ny : op->nx;
+    const int64_t n = dir == 0 ? op->nx : op->ny;
+    DevBuf<uint64_t> keys, keys2;
+    DevBuf<int64_t> idx;
+    keys.alloc(total);
+    keys2.alloc(total);
+    idx.alloc(total);
+    d.close_order.alloc(total);
+    rgfb::k_seg_keys<<<grid_for(total, 256), 256>>>(d.segs.p, d.seg_line.p, total, nl, n,
+                                                    op->nlev, keys.p, idx.p);
+    CUDA_OK(cudaGetLastError());
+    size_t sb = 0;
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(nullptr, sb, keys.p, keys2.p, idx.p, d.close_order.p,
+                                            total));
+    DevBuf<char> st;
+    st.alloc(sb);
+    CUDA_OK(cub::DeviceRadixSort::SortPairs(st.p, sb, keys.p, keys2.p, idx.p, d.close_order.p,
+                                            total));
+  }
   CUDA_OK(cudaDeviceSynchronize());
 }
 
@@ -565,7 +588,7 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})
       b += d->c3.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
-           d->seg_line.bytes();
+           d->seg_line.bytes() + d->close_order.bytes();
     *out = b;
   });
 }

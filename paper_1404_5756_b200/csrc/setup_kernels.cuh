@@ -172,4 +172,19 @@ __global__ void k_seg_fill(const uint8_t* mask, int dir, int64_t nx, int64_t ny,
   }
 }
 
+// Sort key of every segment for the closure pass: (line, end position, level),
+// so the levels sharing a segment end are adjacent (shared closure rows).
+__global__ void k_seg_keys(const int2* segs, const int32_t* seg_line, int64_t nsegs,
+                           int64_t nlines, int64_t n, int64_t nlev, uint64_t* keys,
+                           int64_t* idx) {
+  for (int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; s < nsegs;
+       s += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lg = seg_line[s];
+    const int64_t lev = lg / nlines, line = lg - lev * nlines;
+    const int64_t j = segs[s].x + segs[s].y - 1;
+    keys[s] = static_cast<uint64_t>((line * n + j) * nlev + lev);
+    idx[s] = s;
+  }
+}
+
 }  // namespace rgfb

@@ -57,6 +57,7 @@ struct StreamArgs {
   const int64_t* seg_off;   // per (lev, line) segment prefix offsets
   const int2* segs;         // (start, len)
   const int32_t* seg_line;  // per segment: lev*nlines + line
+  const int64_t* close_order;  // segments sorted by (line, end, level)
   int64_t nsegs;            // segments of this direction (all levels)
   double4* entry;           // [var][nsegs] anti-causal entry states
   const double* pre_scale;  // optional (nlev*nh) input multiplier (variance)

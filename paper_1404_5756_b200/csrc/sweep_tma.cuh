@@ -47,8 +47,9 @@ namespace rgfb {
 // reference's startup rows do at an extended segment's far end.
 template <typename T, int DIR, bool TR>
 __global__ void __launch_bounds__(256) k_close(T* __restrict__ z, StreamArgs a) {
-  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (s >= a.nsegs) return;
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= a.nsegs) return;
+  const int64_t s = __ldg(a.close_order + t);
   const int64_t n = DIR == 0 ? a.nx : a.ny;
   const int64_t nlines = DIR == 0 ? a.ny : a.nx;
   const int64_t nh = a.nx * a.ny;
