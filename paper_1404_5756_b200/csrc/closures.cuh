@@ -14,13 +14,18 @@ namespace rgfb {
 //    (u'_{j+1}, u'_{j+2}, u'_{j+3}) by the causal-transpose gather over the
 //    ghosts, beta scaling, and the anti-causal-transpose gather back.
 // Ghost recursions use the reference's unfused left-to-right order.
+// Output layout: `out` = forward part [nh][10], `out + nh*10` = adjoint part
+// [nh][10] (9 matrix entries, one pad: 80 B rows, TMA-loadable).
 __global__ void k_closures(const Coef3* c3, int64_t nh, int G, double* out, double* scratch,
                            int64_t slab) {
   const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   double* g = scratch + tid * slab;
   for (int64_t p = tid; p < nh; p += (int64_t)gridDim.x * blockDim.x) {
     const Coef3 c = c3[p];
-    double* o = out + p * 18;
+    double* o = out + p * 10;
+    double* oa = out + nh * 10 + p * 10;
+    o[9] = 0.0;
+    oa[9] = 0.0;
     for (int m = 0; m < 3; ++m) {
       // forward closure, basis state e_m over (p_j, p_{j-1}, p_{j-2})
       double pm1 = m == 0, pm2 = m == 1, pm3 = m == 2;
@@ -72,9 +77,9 @@ __global__ void k_closures(const Coef3* c3, int64_t nh, int G, double* out, doub
         w1 = u;
         if (k < 3) s[k] = u;
       }
-      o[9 + 0 + m] = s[0];
-      o[9 + 3 + m] = s[1];
-      o[9 + 6 + m] = s[2];
+      oa[0 + m] = s[0];
+      oa[3 + m] = s[1];
+      oa[6 + m] = s[2];
     }
   }
 }

@@ -135,4 +135,11 @@ struct Coef3 {
   double a1, a2, a3, b;  // 32 B: one sector per point
 };
 
+// Closure table addressing: [class][dir][part][nh][10] doubles
+// (part 0 = forward operator, 1 = adjoint).
+__host__ __device__ __forceinline__ int64_t clos_off(int cls, int dir, int part, int64_t nh,
+                                                     int64_t h) {
+  return ((static_cast<int64_t>(cls) * 2 + dir) * 2 + part) * nh * 10 + h * 10;
+}
+
 }  // namespace rgfb

@@ -168,6 +168,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.words = op->words[dir];
     a.ghost = op->ghost_d.p;
     a.cls = op->cls_d.p;
+    a.nclass = op->nclass;
     a.clos = op->clos.p;
     a.seg_off = d.seg_off.p;
     a.segs = d.segs.p;
@@ -480,7 +481,7 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
         op->nclass = static_cast<int>(classes.size());
         op->cls_d.upload(cls.data(), cls.size());
-        op->clos.alloc(static_cast<size_t>(op->nclass) * 2 * nh * 18);
+        op->clos.alloc(static_cast<size_t>(op->nclass) * 2 * 2 * nh * 10);
         const int threads = 128;
         const int blocks = grid_for(nh, threads, 148 * 8);
         const int64_t slab = op->gmax + 1;
@@ -490,7 +491,7 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
           for (int dir = 0; dir < 2; ++dir) {
             const DirData& d = dir == 0 ? op->dx_ : op->dy_;
             rgfb::k_closures<<<blocks, threads>>>(d.c3.p, nh, static_cast<int>(classes[c]),
-                                                  op->clos.p + (static_cast<int64_t>(c) * 2 + dir) * nh * 18,
+                                                  op->clos.p + rgfb::clos_off(c, dir, 0, nh, 0),
                                                   scr.p, slab);
             CUDA_OK(cudaGetLastError());
           }

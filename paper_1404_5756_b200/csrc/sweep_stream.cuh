@@ -53,6 +53,7 @@ struct StreamArgs {
   int64_t words;            // 64-bit words per line
   const int* ghost;         // per level
   const int* cls;           // per level closure class
+  int nclass;               // distinct ghost widths (classes)
   const double* clos;       // [class][dir][nh][18]: M (9) then adjoint closure (9)
   const int64_t* seg_off;   // per (lev, line) segment prefix offsets
   const int2* segs;         // (start, len)
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(128) k_entries(const T* __restrict__ z, Stream
   const T* zl = z + p * nh + hb;
   const Coef3* C = a.c3 + hb;
   const int G = a.ghost[lev];
-  const double* CL = a.clos + ((int64_t)(a.cls[lev] * 2 + DIR) * nh + hb) * 18 + (TR ? 9 : 0);
+  const double* CL = a.clos + clos_off(a.cls[lev], DIR, TR ? 1 : 0, nh, hb);
   const int64_t s0 = a.seg_off[lev * nlines + line], s1 = a.seg_off[lev * nlines + line + 1];
   double4* E = a.entry + var * a.nsegs;
   for (int64_t s = s0; s < s1; ++s) {
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(128) k_entries(const T* __restrict__ z, Stream
       const double z0 = ldv(zl + j * stride);
       const double z1 = sg.y >= 2 ? ldv(zl + (j - 1) * stride) : 0.0;
       const double z2 = sg.y >= 3 ? ldv(zl + (j - 2) * stride) : 0.0;
-      const double* M = CL + j * stride * 18;
+      const double* M = CL + j * stride * 10;
       double x0 = z0, x1 = z1, x2 = z2;
       if (TR) {
         const Coef3 c = ldc(C + j * stride);

@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(256) k_close(T* __restrict__ z, StreamArgs a) 
   const int G = a.ghost[lev];
   if (!(j < n - 1 && G > 0)) return;  // no right ghosts: zero entry
   const int64_t h = DIR == 0 ? line * a.nx + j : j * a.nx + line;
-  const double* Mp = a.clos + ((int64_t)(a.cls[lev] * 2 + DIR) * nh + h) * 18 + (TR ? 9 : 0);
+  const double* Mp = a.clos + clos_off(a.cls[lev], DIR, TR ? 1 : 0, nh, h);
   double M[9];
 #pragma unroll
   for (int q = 0; q < 9; ++q) M[q] = __ldg(Mp + q);
@@ -188,19 +188,25 @@ struct StageBits {
 };
 
 // ================================================================ y-sweep
-template <typename T, int NW, int U>
+template <typename T, int NW, int U, bool FOLD>
 struct YT {
   static constexpr size_t field = size_t(NW) * U * 32 * sizeof(T);
   static constexpr size_t coef = size_t(U) * 32 * sizeof(Coef3);
   static constexpr size_t idc = size_t(U) * 32 * sizeof(double);
-  static constexpr size_t bytes = field + coef + idc;
+  static constexpr size_t clos = FOLD ? size_t(U) * 32 * 10 * sizeof(double) : 0;
+  static constexpr size_t bytes = field + coef + idc + clos;
 };
 
-template <typename T, bool TR, bool PD, bool IDC, bool VAR, int NW, int U, int S>
+// FOLD (pass A only, one closure class): the right-ghost closure rows are
+// staged with the coefficients, and each segment end's entry is folded into
+// the stored terms of rows j, j-1, j-2 on the fly (a 2-row store delay line
+// keeps j-1 and j-2 in registers), so no raw-state buffer or closure pass.
+template <typename T, bool TR, bool PD, bool IDC, bool VAR, bool FOLD, int NW, int U, int S>
 __global__ void __launch_bounds__(32 * (NW + 1), 1)
     k_ytma(T* __restrict__ out, StreamArgs a, const __grid_constant__ CUtensorMap tm_field,
-           const __grid_constant__ CUtensorMap tm_coef, const __grid_constant__ CUtensorMap tm_idc) {
-  using L = YT<T, NW, U>;
+           const __grid_constant__ CUtensorMap tm_coef, const __grid_constant__ CUtensorMap tm_idc,
+           const __grid_constant__ CUtensorMap tm_clos) {
+  using L = YT<T, NW, U, FOLD>;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // 1024 B alignment by pointer arithmetic (keeps the shared address space)
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -235,7 +241,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       tma_prefetch_desc(&tm_field);
       tma_prefetch_desc(&tm_coef);
       if (need_idc) tma_prefetch_desc(&tm_idc);
-      const uint32_t total = static_cast<uint32_t>(L::field + L::coef + (need_idc ? L::idc : 0));
+      const uint32_t total =
+          static_cast<uint32_t>(L::field + L::coef + (need_idc ? L::idc : 0) + L::clos);
       for (int64_t i = 0; i < nst; ++i) {
         const int s = static_cast<int>(i % S);
         const int64_t m = i / S;
@@ -249,6 +256,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         if (need_idc)
           tma_load_2d(base + L::field + L::coef, &tm_idc, static_cast<int>(ix0), lo, &full[s],
                       pol_keep);
+        if constexpr (FOLD)
+          tma_load_3d(base + L::field + L::coef + L::idc, &tm_clos, 0, static_cast<int>(ix0), lo,
+                      &full[s], pol_keep);
       }
     }
     return;
@@ -272,6 +282,10 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   int64_t sA = s0;      // pass A: next segment index to be closed
   uint32_t carry = 0;   // A: sea(lo-1); D: sea(lo+U)
   (void)s1;
+  // FOLD: stored terms of rows k-1, k-2 (not yet written), the coefficients
+  // feeding their corrections, and the current segment's length so far
+  double d1 = 0.0, d2 = 0.0, pa2 = 0.0, pa3 = 0.0, ppa3 = 0.0;
+  int seglen = 0;
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
@@ -285,7 +299,50 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     const double* id = reinterpret_cast<const double*>(base + L::field + L::coef) + lane;
     T* drow = dst + lo * nx;
     const int rvalid = act ? static_cast<int>(ny - lo < U ? ny - lo : U) : 0;
-    if constexpr (!PD) {
+    if constexpr (!PD && FOLD) {
+      const uint32_t starts = sb & ~((sb << 1) | carry);
+      const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(lo) << (U - 1)));
+      const double* cm = reinterpret_cast<const double*>(base + L::field + L::coef + L::idc) +
+                         lane * 10;
+#pragma unroll
+      for (int r = 0; r < U; ++r) {
+        const int64_t k = lo + r;
+        if ((starts >> r) & 1u) {
+          st.reset();
+          seglen = 0;
+        }
+        ++seglen;
+        double w = static_cast<double>(fld[r * 32]);
+        if (TR) {
+          if constexpr (VAR) w *= __ldg(PRE + k * nx);
+          if constexpr (IDC) w *= id[r * 32];
+        }
+        const Coef3 c = cf[r * 32];
+        double res = c.b * st.step(c, w);  // stored term beta*p / beta*u
+        if (((ends >> r) & 1u) && k < ny - 1) {  // fold the right-ghost entry
+          const double4 rw = st.raw();
+          const double* M = cm + r * 320;
+          const double e1 = fma(M[0], rw.x, fma(M[1], rw.y, M[2] * rw.z));
+          const double e2 = fma(M[3], rw.x, fma(M[4], rw.y, M[5] * rw.z));
+          const double e3 = fma(M[6], rw.x, fma(M[7], rw.y, M[8] * rw.z));
+          res += fma(c.a1, e1, fma(c.a2, e2, c.a3 * e3));
+          if (TR) {  // sources beyond j carry the ghost (= c_j) coefficients
+            if (seglen >= 2) d1 += fma(c.a2, e1, c.a3 * e2);
+            if (seglen >= 3) d2 += c.a3 * e1;
+          } else {
+            if (seglen >= 2) d1 += fma(pa2, e1, pa3 * e2);
+            if (seglen >= 3) d2 += ppa3 * e1;
+          }
+        }
+        if (act && k >= 2 && k - 2 < ny) __stcs(dst + (k - 2) * nx, static_cast<T>(d2));
+        d2 = d1;
+        d1 = res;
+        ppa3 = pa3;
+        pa2 = c.a2;
+        pa3 = c.a3;
+      }
+      carry = (sb >> (U - 1)) & 1u;
+    } else if constexpr (!PD) {
       const uint32_t starts = sb & ~((sb << 1) | carry);
       const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(lo) << (U - 1)));
 #pragma unroll
@@ -322,19 +379,25 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
   }
+  if constexpr (!PD && FOLD) {  // flush the delay line: rows kl-1, kl
+    const int64_t kl = nst * U - 1;
+    if (act && kl - 1 < ny) __stcs(dst + (kl - 1) * nx, static_cast<T>(d2));
+    if (act && kl < ny) __stcs(dst + kl * nx, static_cast<T>(d1));
+  }
 }
 
-constexpr int kYtNW = 16, kYtU = 8, kYtS = 4;
+constexpr int kYtNW = 16, kYtU = 8, kYtS = 4, kYtSFold = 3;
 
 // ================================================================ x-sweep
 // one row, up to 32*NW planes per CTA; U*sizeof(T) = 128 B (swizzle atom)
-template <typename T, int NW>
+template <typename T, int NW, bool FOLD>
 struct XT {
   static constexpr int U = 128 / int(sizeof(T));
   static constexpr size_t field = size_t(NW) * 32 * 128;
   static constexpr size_t coef = size_t(U) * sizeof(Coef3);
   static constexpr size_t idc = size_t(U) * sizeof(double);
-  static constexpr size_t bytes = (field + coef + idc + 1023) / 1024 * 1024;
+  static constexpr size_t clos = FOLD ? size_t(U) * 10 * sizeof(double) : 0;
+  static constexpr size_t bytes = (field + coef + idc + clos + 1023) / 1024 * 1024;
 };
 
 // byte offset of element u of plane-row r in a 128B-swizzled [rows][128 B] tile
@@ -342,12 +405,12 @@ __device__ __forceinline__ uint32_t swz128(int r, uint32_t byte_in_row) {
   return static_cast<uint32_t>(r) * 128u + ((((byte_in_row >> 4) ^ (r & 7)) << 4) | (byte_in_row & 15u));
 }
 
-template <typename T, bool TR, bool PD, bool IDC, bool VAR, int NW, int S>
+template <typename T, bool TR, bool PD, bool IDC, bool VAR, bool FOLD, int NW, int S>
 __global__ void __launch_bounds__(32 * (NW + 1), 1)
     k_xtma(T* __restrict__ out, StreamArgs a, const __grid_constant__ CUtensorMap tm_in,
            const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ CUtensorMap tm_coef,
-           const __grid_constant__ CUtensorMap tm_idc) {
-  using L = XT<T, NW>;
+           const __grid_constant__ CUtensorMap tm_idc, const __grid_constant__ CUtensorMap tm_clos) {
+  using L = XT<T, NW, FOLD>;
   constexpr int U = L::U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   // 1024 B alignment by pointer arithmetic (keeps the shared address space)
@@ -381,7 +444,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
       tma_prefetch_desc(&tm_in);
       tma_prefetch_desc(&tm_coef);
-      const uint32_t total = static_cast<uint32_t>(L::field + L::coef + (need_idc ? L::idc : 0));
+      const uint32_t total =
+          static_cast<uint32_t>(L::field + L::coef + (need_idc ? L::idc : 0) + L::clos);
       for (int64_t i = 0; i < nst; ++i) {
         const int s = static_cast<int>(i % S);
         const int64_t m = i / S;
@@ -395,6 +459,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         if (need_idc)
           tma_load_2d(base + L::field + L::coef, &tm_idc, k0, static_cast<int>(iy), &full[s],
                       pol_keep);
+        if constexpr (FOLD)
+          tma_load_3d(base + L::field + L::coef + L::idc, &tm_clos, 0, k0, static_cast<int>(iy),
+                      &full[s], pol_keep);
       }
     }
     return;
@@ -416,6 +483,15 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   int64_t sA = s0;
   uint32_t carry = 0;  // A: sea(k0-1); D: sea(k0+U)
   (void)s1;
+  // FOLD: stored terms of elements k-1, k-2 (not yet written back), the
+  // coefficients feeding their corrections, current segment length
+  double d1 = 0.0, d2 = 0.0, pa2 = 0.0, pa3 = 0.0, ppa3 = 0.0;
+  int seglen = 0;
+  constexpr int ESZ = static_cast<int>(sizeof(T));
+  constexpr int EPCX = 16 / ESZ;
+  auto elem = [&](unsigned char* tile_row, int u) -> T* {  // swizzled element address
+    return reinterpret_cast<T*>(tile_row + (((u / EPCX) ^ (pr & 7)) << 4) + (u % EPCX) * ESZ);
+  };
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
@@ -430,7 +506,50 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     constexpr int EPC = 16 / int(sizeof(T));  // elements per 16 B chunk
     unsigned char* rowp = base + pr * 128;
     const int sw = pr & 7;
-    if constexpr (!PD) {
+    if constexpr (!PD && FOLD) {
+      const uint32_t starts = sb & ~((sb << 1) | carry);
+      const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(k0) << (U - 1)));
+      const double* cm = reinterpret_cast<const double*>(base + L::field + L::coef + L::idc);
+      unsigned char* prow = smem + ((i + S - 1) % S) * L::bytes + pr * 128;  // previous tile
+#pragma unroll 4
+      for (int u = 0; u < U; ++u) {
+        const int64_t k = k0 + u;
+        if ((starts >> u) & 1u) {
+          st.reset();
+          seglen = 0;
+        }
+        ++seglen;
+        double w = static_cast<double>(*elem(rowp, u));
+        if (TR) {
+          if constexpr (VAR) w *= __ldg(PRE + k);
+          if constexpr (IDC) w *= id[u];
+        }
+        const Coef3 c = cf[u];
+        double res = c.b * st.step(c, w);
+        if (((ends >> u) & 1u) && k < n - 1) {  // fold the right-ghost entry
+          const double4 rw = st.raw();
+          const double* M = cm + u * 10;
+          const double e1 = fma(M[0], rw.x, fma(M[1], rw.y, M[2] * rw.z));
+          const double e2 = fma(M[3], rw.x, fma(M[4], rw.y, M[5] * rw.z));
+          const double e3 = fma(M[6], rw.x, fma(M[7], rw.y, M[8] * rw.z));
+          res += fma(c.a1, e1, fma(c.a2, e2, c.a3 * e3));
+          if (TR) {
+            if (seglen >= 2) d1 += fma(c.a2, e1, c.a3 * e2);
+            if (seglen >= 3) d2 += c.a3 * e1;
+          } else {
+            if (seglen >= 2) d1 += fma(pa2, e1, pa3 * e2);
+            if (seglen >= 3) d2 += ppa3 * e1;
+          }
+        }
+        if (k >= 2) *(u >= 2 ? elem(rowp, u - 2) : elem(prow, U + u - 2)) = static_cast<T>(d2);
+        d2 = d1;
+        d1 = res;
+        ppa3 = pa3;
+        pa2 = c.a2;
+        pa3 = c.a3;
+      }
+      carry = (sb >> (U - 1)) & 1u;
+    } else if constexpr (!PD) {
       const uint32_t starts = sb & ~((sb << 1) | carry);
       const uint32_t ends = sb & ~((sb >> 1) | (sbw.after<U>(k0) << (U - 1)));
 #pragma unroll 1
@@ -513,15 +632,38 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     // all consumers' results in smem -> one TMA store of the box
     fence_proxy_async_smem();
     asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NW) : "memory");
-    if (threadIdx.x == 0) {
-      tma_store_3d(&tm_out, static_cast<int>(k0), static_cast<int>(iy), static_cast<int>(p0), base,
-                   l2_evict_first());
-      bulk_commit();
-      // the stage is free once the store has read it (the previous stage's
-      // store is older; wait for it before releasing that stage)
-      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
-      if (i > 0) mbar_arrive(&empty[(i - 1) % S]);
+    if constexpr (!PD && FOLD) {
+      // the last two elements of a tile are final only after the next
+      // stage's first two steps: store the previous stage's tile
+      if (threadIdx.x == 0 && i > 0) {
+        tma_store_3d(&tm_out, static_cast<int>(k0 - U), static_cast<int>(iy),
+                     static_cast<int>(p0), smem + ((i - 1) % S) * L::bytes, l2_evict_first());
+        bulk_commit();
+        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        if (i > 1) mbar_arrive(&empty[(i - 2) % S]);
+      }
+    } else {
+      if (threadIdx.x == 0) {
+        tma_store_3d(&tm_out, static_cast<int>(k0), static_cast<int>(iy), static_cast<int>(p0),
+                     base, l2_evict_first());
+        bulk_commit();
+        // the stage is free once the store has read it (the previous stage's
+        // store is older; wait for it before releasing that stage)
+        asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+        if (i > 0) mbar_arrive(&empty[(i - 1) % S]);
+      }
     }
+  }
+  if constexpr (!PD && FOLD) {  // flush the delay line into the last tile and store it
+    unsigned char* lrow = smem + ((nst - 1) % S) * L::bytes + pr * 128;
+    *elem(lrow, U - 2) = static_cast<T>(d2);
+    *elem(lrow, U - 1) = static_cast<T>(d1);
+    fence_proxy_async_smem();
+    asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NW) : "memory");
+    if (threadIdx.x == 0)
+      tma_store_3d(&tm_out, static_cast<int>((nst - 1) * U), static_cast<int>(iy),
+                   static_cast<int>(p0), smem + ((nst - 1) % S) * L::bytes, l2_evict_first());
+    if (threadIdx.x == 0) bulk_commit();
   }
   if (threadIdx.x == 0) bulk_wait_all();
 }
@@ -535,13 +677,13 @@ inline bool tma_supported(const T* in, const T* out, int64_t nx) {
          reinterpret_cast<uintptr_t>(in) % 16 == 0 && reinterpret_cast<uintptr_t>(out) % 16 == 0;
 }
 
-template <typename T, bool TR, bool PD, bool IDC, bool VAR>
+template <typename T, bool TR, bool PD, bool IDC, bool VAR, bool FOLD>
 void launch_ytma_k(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
-  constexpr int NW = kYtNW, U = kYtU, S = kYtS;
-  const size_t smem = S * YT<T, NW, U>::bytes + 2 * S * sizeof(uint64_t) + 1024;
+  constexpr int NW = kYtNW, U = kYtU, S = FOLD ? kYtSFold : kYtS;
+  const size_t smem = S * YT<T, NW, U, FOLD>::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_ytma<T, TR, PD, IDC, VAR, NW, U, S>,
+    cudaFuncSetAttribute(k_ytma<T, TR, PD, IDC, VAR, FOLD, NW, U, S>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
@@ -563,18 +705,27 @@ void launch_ytma_k(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const CUtensorMap ti = a.idc ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
                                            CU_TENSOR_MAP_SWIZZLE_NONE)
                                : tc;
+  CUtensorMap tcl = tc;
+  if (FOLD) {  // closure rows of class 0, this direction/part: [ny][nx][10]
+    const uint64_t md[3] = {10, uint64_t(a.nx), uint64_t(a.ny)};
+    const uint64_t ms[2] = {80, uint64_t(a.nx) * 80};
+    const uint32_t mb[3] = {10, 32, U};
+    tcl = make_tmap(a.clos + clos_off(0, 1, TR ? 1 : 0, a.nx * a.ny, 0),
+                    CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, md, ms, mb, CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
   const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NW - 1) / NW);
-  k_ytma<T, TR, PD, IDC, VAR, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tf, tc, ti);
+  k_ytma<T, TR, PD, IDC, VAR, FOLD, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tf, tc,
+                                                                                  ti, tcl);
 }
 
-template <typename T, bool TR, bool PD, bool IDC, bool VAR>
+template <typename T, bool TR, bool PD, bool IDC, bool VAR, bool FOLD>
 void launch_xtma_k(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   constexpr int NW = kXtNW, S = kXtS;
-  using L = XT<T, NW>;
+  using L = XT<T, NW, FOLD>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_xtma<T, TR, PD, IDC, VAR, NW, S>,
+    cudaFuncSetAttribute(k_xtma<T, TR, PD, IDC, VAR, FOLD, NW, S>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
@@ -600,60 +751,88 @@ void launch_xtma_k(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const CUtensorMap ti = a.idc ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
                                            CU_TENSOR_MAP_SWIZZLE_NONE)
                                : tc;
+  CUtensorMap tcl = tc;
+  if (FOLD) {
+    const uint64_t md[3] = {10, uint64_t(a.nx), uint64_t(a.ny)};
+    const uint64_t ms[2] = {80, uint64_t(a.nx) * 80};
+    const uint32_t mb[3] = {10, uint32_t(L::U), 1};
+    tcl = make_tmap(a.clos + clos_off(0, 0, TR ? 1 : 0, a.nx * a.ny, 0),
+                    CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, md, ms, mb, CU_TENSOR_MAP_SWIZZLE_NONE);
+  }
   const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
   const int64_t blocks = a.ny * PB;
-  k_xtma<T, TR, PD, IDC, VAR, NW, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tin, tout, tc,
-                                                                          ti);
+  k_xtma<T, TR, PD, IDC, VAR, FOLD, NW, S><<<blocks, 32 * (NW + 1), smem, st>>>(out, a, tin, tout,
+                                                                                tc, ti, tcl);
 }
 
 // runtime flags -> template flags
-template <typename T, bool TR, bool PD>
+template <typename T, bool TR, bool PD, bool FOLD>
 void launch_ytma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const bool idc = a.idc != nullptr && (PD ? !TR : TR);
   const bool var = PD ? a.post_scale != nullptr : (TR && a.pre_scale != nullptr);
   if (idc) {
-    if (var) launch_ytma_k<T, TR, PD, true, true>(in, out, a, st);
-    else launch_ytma_k<T, TR, PD, true, false>(in, out, a, st);
+    if (var) launch_ytma_k<T, TR, PD, true, true, FOLD>(in, out, a, st);
+    else launch_ytma_k<T, TR, PD, true, false, FOLD>(in, out, a, st);
   } else {
-    if (var) launch_ytma_k<T, TR, PD, false, true>(in, out, a, st);
-    else launch_ytma_k<T, TR, PD, false, false>(in, out, a, st);
+    if (var) launch_ytma_k<T, TR, PD, false, true, FOLD>(in, out, a, st);
+    else launch_ytma_k<T, TR, PD, false, false, FOLD>(in, out, a, st);
   }
 }
-template <typename T, bool TR, bool PD>
+template <typename T, bool TR, bool PD, bool FOLD>
 void launch_xtma(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const bool idc = a.idc != nullptr && (PD ? !TR : TR);
   const bool var = PD ? a.post_scale != nullptr : (TR && a.pre_scale != nullptr);
   if (idc) {
-    if (var) launch_xtma_k<T, TR, PD, true, true>(in, out, a, st);
-    else launch_xtma_k<T, TR, PD, true, false>(in, out, a, st);
+    if (var) launch_xtma_k<T, TR, PD, true, true, FOLD>(in, out, a, st);
+    else launch_xtma_k<T, TR, PD, true, false, FOLD>(in, out, a, st);
   } else {
-    if (var) launch_xtma_k<T, TR, PD, false, true>(in, out, a, st);
-    else launch_xtma_k<T, TR, PD, false, false>(in, out, a, st);
+    if (var) launch_xtma_k<T, TR, PD, false, true, FOLD>(in, out, a, st);
+    else launch_xtma_k<T, TR, PD, false, false, FOLD>(in, out, a, st);
   }
 }
 
 template <typename T>
 int launch_tma_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const int64_t cblocks = (a.nsegs + 255) / 256;
+  if (a.nclass == 1) {  // fused closure (single ghost-width class)
+    if (a.dir == 1) {
+      if (a.transpose) {
+        launch_ytma<T, true, false, true>(in, out, a, st);
+        launch_ytma<T, true, true, false>(out, out, a, st);
+      } else {
+        launch_ytma<T, false, false, true>(in, out, a, st);
+        launch_ytma<T, false, true, false>(out, out, a, st);
+      }
+    } else {
+      if (a.transpose) {
+        launch_xtma<T, true, false, true>(in, out, a, st);
+        launch_xtma<T, true, true, false>(out, out, a, st);
+      } else {
+        launch_xtma<T, false, false, true>(in, out, a, st);
+        launch_xtma<T, false, true, false>(out, out, a, st);
+      }
+    }
+    return 2;
+  }
   if (a.dir == 1) {
     if (a.transpose) {
-      launch_ytma<T, true, false>(in, out, a, st);
+      launch_ytma<T, true, false, false>(in, out, a, st);
       k_close<T, 1, true><<<cblocks, 256, 0, st>>>(out, a);
-      launch_ytma<T, true, true>(out, out, a, st);
+      launch_ytma<T, true, true, false>(out, out, a, st);
     } else {
-      launch_ytma<T, false, false>(in, out, a, st);
+      launch_ytma<T, false, false, false>(in, out, a, st);
       k_close<T, 1, false><<<cblocks, 256, 0, st>>>(out, a);
-      launch_ytma<T, false, true>(out, out, a, st);
+      launch_ytma<T, false, true, false>(out, out, a, st);
     }
   } else {
     if (a.transpose) {
-      launch_xtma<T, true, false>(in, out, a, st);
+      launch_xtma<T, true, false, false>(in, out, a, st);
       k_close<T, 0, true><<<cblocks, 256, 0, st>>>(out, a);
-      launch_xtma<T, true, true>(out, out, a, st);
+      launch_xtma<T, true, true, false>(out, out, a, st);
     } else {
-      launch_xtma<T, false, false>(in, out, a, st);
+      launch_xtma<T, false, false, false>(in, out, a, st);
       k_close<T, 0, false><<<cblocks, 256, 0, st>>>(out, a);
-      launch_xtma<T, false, true>(out, out, a, st);
+      launch_xtma<T, false, true, false>(out, out, a, st);
     }
   }
   return 3;

@@ -296,3 +296,17 @@ def test_streaming_vs_exact_path(P, monkeypatch):
         got = fast.apply(getattr(P, name), f)
         want = cpu.apply(getattr(O, name), f)
         assert relmax(got, want) <= TOL64, (name, relmax(got, want))
+
+
+@pytest.mark.parametrize("sea", [0.45, 0.7])
+def test_short_segments_tma_paths(P, sea):
+    """Many length-1/2 segments (corrections at j-1, j-2 skipped), segment ends
+    on stage boundaries, aligned rows (TMA paths, fused closure)."""
+    g, rx, ry = random_case(900 + int(sea * 100), nx=96, ny=40, nlev=2, sea=sea)
+    gpu, cpu = build_pair(P, g, rx, ry)
+    f = np.random.default_rng(12).standard_normal((2, 40, 96))
+    for name in ("GX", "GY", "GXT", "GYT", "B"):
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
+        assert np.all(got[~g["mask"]] == 0.0)
