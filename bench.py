@@ -73,7 +73,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -107,6 +107,17 @@ class ClockSampler:
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
                 "samples": len(self.rows)}
+
+
+def measured_traffic(cfg_name, dtype, order, kernel):
+    """ncu DRAM bytes (read + write) per launch of the dominant sweep, from
+    the committed capture summary (profiles/traffic.json); None if absent."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            t = json.load(f)
+        return t[f"{cfg_name}/{dtype}/{order}"][kernel]
+    except Exception:
+        return None
 
 
 def dist_init():
@@ -316,7 +327,9 @@ def main():
                        "l2": "inputs larger than L2 (field >> 126 MB)",
                        "options": "unit_dc=1 yvv95 ghost=ceil(9 max sigma) per level"},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None,
+                         "frac": achieved / peak,
+                         "traffic": measured_traffic(args.config, args.dtype, args.order,
+                                                     f"{dom}-sweep"),
                          "kernel": f"{dom}-sweep", "peak_source": peak_src,
                          "bytes_per_launch": bytes_sweep,
                          "xy_bytes_alg_GBs": xy_gbs, "xy_frac": xy_gbs / peak},
