@@ -134,10 +134,28 @@ struct rgf_op {
   DevBuf<double> clos;  // [class][dir][nh][18]
   DevBuf<double4> entry;  // [var][segments] anti-causal entry states (apply scratch)
   int nclass = 0;
+  // host-apply pipeline: H2D / compute / D2H streams, per-slot chunk buffers
+  cudaStream_t pipe_stream[3] = {nullptr, nullptr, nullptr};
+  cudaEvent_t pipe_ev[3][3] = {};
+  cudaEvent_t pipe_ev_user = nullptr;
+  DevBuf<char> pin[3], pout[3];
+  void pipe_init() {
+    if (pipe_stream[0]) return;
+    for (auto& s : pipe_stream) CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
+    for (auto& row : pipe_ev)
+      for (auto& e : row) CUDA_OK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CUDA_OK(cudaEventCreateWithFlags(&pipe_ev_user, cudaEventDisableTiming));
+  }
   std::mutex mu;  // apply() is const in the reference; serialize buffer reuse
 
   ~rgf_op() {
     if (own_stream) cudaStreamDestroy(own_stream);
+    for (auto s : pipe_stream)
+      if (s) cudaStreamDestroy(s);
+    for (auto& row : pipe_ev)
+      for (auto e : row)
+        if (e) cudaEventDestroy(e);
+    if (pipe_ev_user) cudaEventDestroy(pipe_ev_user);
   }
 };
 
@@ -149,9 +167,9 @@ namespace {
 // (the variance multiplies of apply_v / apply_v_transpose).
 template <typename T>
 void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nvar,
-           const double* pre, const double* post, cudaStream_t st) {
+           int64_t lev0, int64_t nlev, const double* pre, const double* post, cudaStream_t st) {
   const DirData& d = dir == 0 ? op->dx_ : op->dy_;
-  const int64_t lines = nvar * op->nlev * (dir == 0 ? op->ny : op->nx);
+  const int64_t lines = nvar * nlev * (dir == 0 ? op->ny : op->nx);
 
   if (op->stream_ok) {
     rgfb::StreamArgs a{};
@@ -160,7 +178,8 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.unit_dc = op->unit_dc;
     a.nx = op->nx;
     a.ny = op->ny;
-    a.nlev = op->nlev;
+    a.nlev = nlev;
+    a.lev0 = lev0;
     a.nvar = nvar;
     a.c3 = d.c3.p;
     a.idc = op->unit_dc ? d.idc.p : nullptr;
@@ -201,7 +220,8 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
   a.unit_dc = op->unit_dc;
   a.nx = op->nx;
   a.ny = op->ny;
-  a.nlev = op->nlev;
+  a.nlev = nlev;
+  a.lev0 = lev0;
   a.nvar = nvar;
   a.c3 = d.c3.p;
   a.c1 = d.c1.p;
@@ -220,47 +240,106 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
 }
 
 template <typename T>
-void apply_typed(rgf_op* op, int kind, const T* in, T* out, int64_t nvar, cudaStream_t st) {
-  const size_t count = static_cast<size_t>(nvar * op->nlev * op->nx * op->ny);
+void apply_typed(rgf_op* op, int kind, const T* in, T* out, int64_t nvar, int64_t lev0,
+                 int64_t nlev, cudaStream_t st) {
+  const size_t count = static_cast<size_t>(nvar * nlev * op->nx * op->ny);
   const double* var = op->has_variance ? op->variance.p : nullptr;
   auto tmp = [&](DevBuf<char>& b) {
     b.alloc(count * sizeof(T));
     return reinterpret_cast<T*>(b.p);
   };
+  auto sw = [&](int dir, bool tr, const T* i, T* o, const double* pre, const double* post) {
+    sweep<T>(op, dir, tr, i, o, nvar, lev0, nlev, pre, post, st);
+  };
   switch (kind) {
-    case RGF_GX: sweep<T>(op, 0, false, in, out, nvar, nullptr, nullptr, st); break;
-    case RGF_GY: sweep<T>(op, 1, false, in, out, nvar, nullptr, nullptr, st); break;
-    case RGF_GXT: sweep<T>(op, 0, true, in, out, nvar, nullptr, nullptr, st); break;
-    case RGF_GYT: sweep<T>(op, 1, true, in, out, nvar, nullptr, nullptr, st); break;
+    case RGF_GX: sw(0, false, in, out, nullptr, nullptr); break;
+    case RGF_GY: sw(1, false, in, out, nullptr, nullptr); break;
+    case RGF_GXT: sw(0, true, in, out, nullptr, nullptr); break;
+    case RGF_GYT: sw(1, true, in, out, nullptr, nullptr); break;
     case RGF_GYGX: {
       T* t = tmp(op->tmp1);
-      sweep<T>(op, 0, false, in, t, nvar, nullptr, nullptr, st);
-      sweep<T>(op, 1, false, t, out, nvar, nullptr, nullptr, st);
+      sw(0, false, in, t, nullptr, nullptr);
+      sw(1, false, t, out, nullptr, nullptr);
       break;
     }
     case RGF_V: {  // covariance.cpp:382-387: diag(var) G_y G_x
       T* t = tmp(op->tmp1);
-      sweep<T>(op, 0, false, in, t, nvar, nullptr, nullptr, st);
-      sweep<T>(op, 1, false, t, out, nvar, nullptr, var, st);
+      sw(0, false, in, t, nullptr, nullptr);
+      sw(1, false, t, out, nullptr, var);
       break;
     }
     case RGF_VT: {  // covariance.cpp:389-394: G_x^T G_y^T diag(var)
       T* t = tmp(op->tmp1);
-      sweep<T>(op, 1, true, in, t, nvar, var, nullptr, st);
-      sweep<T>(op, 0, true, t, out, nvar, nullptr, nullptr, st);
+      sw(1, true, in, t, var, nullptr);
+      sw(0, true, t, out, nullptr, nullptr);
       break;
     }
     case RGF_B: {  // covariance.cpp:396-398: V V^T
       T* t = tmp(op->tmp1);
       T* u = tmp(op->tmp2);
-      sweep<T>(op, 1, true, in, t, nvar, var, nullptr, st);
-      sweep<T>(op, 0, true, t, u, nvar, nullptr, nullptr, st);
-      sweep<T>(op, 0, false, u, t, nvar, nullptr, nullptr, st);
-      sweep<T>(op, 1, false, t, out, nvar, nullptr, var, st);
+      sw(1, true, in, t, var, nullptr);
+      sw(0, true, t, u, nullptr, nullptr);
+      sw(0, false, u, t, nullptr, nullptr);
+      sw(1, false, t, out, nullptr, var);
       break;
     }
     default: throw InvalidArgument("apply: unknown operator kind");
   }
+}
+
+// Host-memory apply as a level-chunked pipeline: chunk c's H2D copy, its
+// sweeps and its D2H copy run on three streams, so PCIe traffic in both
+// directions overlaps the kernels of neighbouring chunks (levels are
+// independent 2-D problems). Pinned host buffers give full overlap; pageable
+// ones still work (the copies then serialise through staging).
+template <typename T>
+void apply_host_pipelined(rgf_op* op, int kind, const T* hin, T* hout, int64_t nvar,
+                          cudaStream_t user) {
+  const int64_t nh = op->nx * op->ny;
+  const int64_t nlev = op->nlev;
+  // ~256 MB per chunk, >= 1 level; at least 4 chunks per variable when possible
+  const int64_t per_level = nh * static_cast<int64_t>(sizeof(T));
+  int64_t chunk_mb = 256;
+  if (const char* e = std::getenv("RGF_B200_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));
+  int64_t cl = std::max<int64_t>(1, (chunk_mb << 20) / per_level);
+  cl = std::min(cl, std::max<int64_t>(1, (nlev + 3) / 4));
+  cl = std::min(cl, nlev);
+  constexpr int kSlots = 3;
+  op->pipe_init();
+  const size_t slot_bytes = static_cast<size_t>(cl * nh) * sizeof(T);
+  for (int sl = 0; sl < kSlots; ++sl) {
+    op->pin[sl].alloc(slot_bytes);
+    op->pout[sl].alloc(slot_bytes);
+  }
+  cudaStream_t h2d = op->pipe_stream[0], cs = op->pipe_stream[1], d2h = op->pipe_stream[2];
+  // order after the caller's prior work on its stream
+  CUDA_OK(cudaEventRecord(op->pipe_ev_user, user));
+  CUDA_OK(cudaStreamWaitEvent(h2d, op->pipe_ev_user, 0));
+  CUDA_OK(cudaStreamWaitEvent(cs, op->pipe_ev_user, 0));
+  int64_t c = 0;
+  for (int64_t v = 0; v < nvar; ++v)
+    for (int64_t l0 = 0; l0 < nlev; l0 += cl, ++c) {
+      const int64_t nl = std::min(cl, nlev - l0);
+      const int sl = static_cast<int>(c % kSlots);
+      const size_t off = static_cast<size_t>((v * nlev + l0) * nh);
+      const size_t bytes = static_cast<size_t>(nl * nh) * sizeof(T);
+      T* din = reinterpret_cast<T*>(op->pin[sl].p);
+      T* dout = reinterpret_cast<T*>(op->pout[sl].p);
+      cudaEvent_t* ev = op->pipe_ev[sl];  // 0: loaded, 1: computed, 2: drained
+      // slot reuse: din is free once the chunk kSlots back was computed,
+      // dout once it was drained
+      if (c >= kSlots) CUDA_OK(cudaStreamWaitEvent(h2d, ev[1], 0));
+      CUDA_OK(cudaMemcpyAsync(din, hin + off, bytes, cudaMemcpyHostToDevice, h2d));
+      CUDA_OK(cudaEventRecord(ev[0], h2d));
+      CUDA_OK(cudaStreamWaitEvent(cs, ev[0], 0));
+      if (c >= kSlots) CUDA_OK(cudaStreamWaitEvent(cs, ev[2], 0));
+      apply_typed<T>(op, kind, din, dout, 1, l0, nl, cs);
+      CUDA_OK(cudaEventRecord(ev[1], cs));
+      CUDA_OK(cudaStreamWaitEvent(d2h, ev[1], 0));
+      CUDA_OK(cudaMemcpyAsync(hout + off, dout, bytes, cudaMemcpyDeviceToHost, d2h));
+      CUDA_OK(cudaEventRecord(ev[2], d2h));
+    }
+  CUDA_OK(cudaStreamSynchronize(d2h));
 }
 
 unsigned long long read_u64(const unsigned long long* d) {
@@ -537,31 +616,24 @@ int rgf_op_apply(rgf_op* op, int kind, int dtype, const void* in, void* out, int
     if (kind < RGF_GX || kind > RGF_GYGX) throw InvalidArgument("apply: unknown operator kind");
     std::lock_guard<std::mutex> lock(op->mu);
     CUDA_OK(cudaSetDevice(op->device));
-    const size_t esz = dtype == RGF_F64 ? 8 : 4;
-    const size_t count = static_cast<size_t>(nvar * op->nlev * op->nx * op->ny);
     // NULL = the legacy default stream (torch's default stream hands us 0)
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const void* din = in;
-    void* dout = out;
     if (memory == RGF_HOST) {
-      op->in_d.alloc(count * esz);
-      op->out_d.alloc(count * esz);
-      CUDA_OK(cudaMemcpyAsync(op->in_d.p, in, count * esz, cudaMemcpyHostToDevice, st));
-      din = op->in_d.p;
-      dout = op->out_d.p;
-    } else if (memory != RGF_DEVICE) {
-      throw InvalidArgument("apply: unknown memory kind");
+      if (dtype == RGF_F64)
+        apply_host_pipelined<double>(op, kind, static_cast<const double*>(in),
+                                     static_cast<double*>(out), nvar, st);
+      else
+        apply_host_pipelined<float>(op, kind, static_cast<const float*>(in),
+                                    static_cast<float*>(out), nvar, st);
+      return;
     }
+    if (memory != RGF_DEVICE) throw InvalidArgument("apply: unknown memory kind");
     if (dtype == RGF_F64)
-      apply_typed<double>(op, kind, static_cast<const double*>(din), static_cast<double*>(dout),
-                          nvar, st);
+      apply_typed<double>(op, kind, static_cast<const double*>(in), static_cast<double*>(out),
+                          nvar, 0, op->nlev, st);
     else
-      apply_typed<float>(op, kind, static_cast<const float*>(din), static_cast<float*>(dout),
-                         nvar, st);
-    if (memory == RGF_HOST) {
-      CUDA_OK(cudaMemcpyAsync(out, dout, count * esz, cudaMemcpyDeviceToHost, st));
-      CUDA_OK(cudaStreamSynchronize(st));
-    }
+      apply_typed<float>(op, kind, static_cast<const float*>(in), static_cast<float*>(out), nvar,
+                         0, op->nlev, st);
   });
 }
 
@@ -585,6 +657,8 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
   return guarded([&] {
     if (!op || !out) throw InvalidArgument("device_bytes: null argument");
     uint64_t b = op->ghost_d.bytes() + op->variance.bytes() + op->in_d.bytes() +
+                 op->pin[0].bytes() + op->pin[1].bytes() + op->pin[2].bytes() +
+                 op->pout[0].bytes() + op->pout[1].bytes() + op->pout[2].bytes() +
                  op->bits[0].bytes() + op->bits[1].bytes() + op->clos.bytes() + op->cls_d.bytes() + op->entry.bytes() +
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})

@@ -18,6 +18,7 @@ struct SweepArgs {
   int k;          // 1st-RF iterations
   int unit_dc;    // 3rd-RF unit-DC rescaling
   int64_t nx, ny, nlev, nvar;
+  int64_t lev0;   // first global level of this launch (level-chunked host pipeline)
   const Coef3* c3;     // rf3 table (dir's), nx*ny
   const double2* c1;   // rf1 table {alpha, beta}
   const double* idc;   // inv_dc table
@@ -188,15 +189,16 @@ __global__ void k_sweep_generic(const T* __restrict__ in, T* __restrict__ out, S
     const int64_t lev = rem / lines_per_level;
     const int64_t line = rem - lev * lines_per_level;
     const int64_t plane = (var * a.nlev + lev) * nh;
+    const int64_t glev = a.lev0 + lev;  // metadata are indexed by global level
     const int64_t hbase = a.dir == 0 ? line * a.nx : line;  // horizontal flat index of k=0
     const int64_t stride = a.dir == 0 ? 1 : a.nx;
     const T* src = in + plane + hbase;
     T* dst = out + plane + hbase;
-    const double* pre = a.pre_scale ? a.pre_scale + lev * nh + hbase : nullptr;
-    const double* post = a.post_scale ? a.post_scale + lev * nh + hbase : nullptr;
-    const int64_t G = a.ghost[lev];
-    const int64_t s0 = a.seg_off[lev * lines_per_level + line];
-    const int64_t s1 = a.seg_off[lev * lines_per_level + line + 1];
+    const double* pre = a.pre_scale ? a.pre_scale + glev * nh + hbase : nullptr;
+    const double* post = a.post_scale ? a.post_scale + glev * nh + hbase : nullptr;
+    const int64_t G = a.ghost[glev];
+    const int64_t s0 = a.seg_off[glev * lines_per_level + line];
+    const int64_t s1 = a.seg_off[glev * lines_per_level + line + 1];
 
     int64_t cursor = 0;  // land before the next segment stays exactly 0
     for (int64_t s = s0; s < s1; ++s) {

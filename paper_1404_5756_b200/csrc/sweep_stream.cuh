@@ -47,6 +47,7 @@ namespace rgfb {
 struct StreamArgs {
   int dir, transpose, unit_dc;
   int64_t nx, ny, nlev, nvar;
+  int64_t lev0;             // first global level of this launch
   const Coef3* c3;
   const double* idc;
   const uint64_t* bits;     // bit-packed masks for this direction
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(128) k_entries(const T* __restrict__ z, Stream
   // plane-fastest: the planes of one line share its closure rows in L2
   const int64_t line = tid / planes;
   const int64_t p = tid - line * planes;
-  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
   const int64_t hb = DIR == 0 ? line * a.nx : line;
   const T* zl = z + p * nh + hb;
   const Coef3* C = a.c3 + hb;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(128) k_y_pass_a(const T* __restrict__ in, T* _
     const int64_t p = g * L + l;
     on[l] = p < planes;
     const int64_t pp = on[l] ? p : planes - 1;
-    const int64_t lev = pp % a.nlev;
+    const int64_t lev = a.lev0 + pp % a.nlev;
     src[l] = in + pp * nh + ix;
     dst[l] = out + pp * nh + ix;
     W[l] = a.bits + (lev * nx + ix) * a.words;
@@ -289,7 +290,7 @@ __global__ void __launch_bounds__(128) k_y_pass_d(T* __restrict__ out, StreamArg
     const int64_t p = g * L + l;
     on[l] = p < planes;
     const int64_t pp = on[l] ? p : planes - 1;
-    const int64_t var = pp / a.nlev, lev = pp - var * a.nlev;
+    const int64_t var = pp / a.nlev, lev = a.lev0 + (pp - var * a.nlev);
     dst[l] = out + pp * nh + ix;
     W[l] = a.bits + (lev * nx + ix) * a.words;
     POST[l] = a.post_scale ? a.post_scale + lev * nh + ix : nullptr;
@@ -393,7 +394,7 @@ __global__ void __launch_bounds__(128) k_x_pass_a(const T* __restrict__ in, T* _
   const bool on = tid < planes * ny;
   const int64_t t = on ? tid : planes * ny - 1;
   const int64_t iy = t / planes, p = t - iy * planes;
-  const int64_t lev = p % a.nlev;
+  const int64_t lev = a.lev0 + p % a.nlev;
   const int64_t hb = iy * n;
   const T* src = on ? in + p * nh + hb : nullptr;
   T* dst = out + p * nh + hb;
@@ -467,7 +468,7 @@ __global__ void __launch_bounds__(128) k_x_pass_d(T* __restrict__ out, StreamArg
   const bool on = tid < planes * ny;
   const int64_t t = on ? tid : planes * ny - 1;
   const int64_t iy = t / planes, p = t - iy * planes;
-  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
   const int64_t hb = iy * n;
   T* dst = on ? out + p * nh + hb : nullptr;
   const Coef3* C = a.c3 + hb;

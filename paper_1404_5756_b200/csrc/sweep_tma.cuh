@@ -56,6 +56,7 @@ __global__ void __launch_bounds__(256) k_close(T* __restrict__ z, StreamArgs a) 
   const int64_t stride = DIR == 0 ? 1 : a.nx;
   const int64_t lg = __ldg(a.seg_line + s);
   const int64_t lev = lg / nlines, line = lg - lev * nlines;
+  if (lev < a.lev0 || lev >= a.lev0 + a.nlev) return;  // level outside this launch
   const int2 sg = __ldg(a.segs + s);
   const int64_t j = sg.x + sg.y - 1;
   const int G = a.ghost[lev];
@@ -76,7 +77,7 @@ __global__ void __launch_bounds__(256) k_close(T* __restrict__ z, StreamArgs a) 
     const double e1 = fma(M[0], r.x, fma(M[1], r.y, M[2] * r.z));
     const double e2 = fma(M[3], r.x, fma(M[4], r.y, M[5] * r.z));
     const double e3 = fma(M[6], r.x, fma(M[7], r.y, M[8] * r.z));
-    T* zl = z + ((v * a.nlev + lev) * nh + h);
+    T* zl = z + ((v * a.nlev + (lev - a.lev0)) * nh + h);
     *zl = static_cast<T>(static_cast<double>(*zl) +
                          fma(cj.a1, e1, fma(cj.a2, e2, cj.a3 * e3)));
     if (sg.y >= 2)
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 
   // consumer: chain (plane p0+warp, column ix0+lane)
   const int64_t p = p0 + warp;
-  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
   const bool act = lane < ncol;
   const int64_t ix = ix0 + (act ? lane : 0);
   T* dst = out + p * nh + ix;
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const int pr = warp * 32 + lane;  // row of the smem tile
   const bool act = pr < npl;
   const int64_t p = p0 + (act ? pr : 0);
-  const int64_t var = p / a.nlev, lev = p - var * a.nlev;
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
   const uint64_t* W = a.bits + (lev * ny + iy) * a.words;
   const double* PRE = (VAR && !PD && TR) ? a.pre_scale + lev * nh + iy * n : nullptr;
   const double* POST = (VAR && PD) ? a.post_scale + lev * nh + iy * n : nullptr;
