@@ -23,6 +23,7 @@
 #include "sweep_generic.cuh"
 #include "sweep_stream.cuh"
 #include "sweep_tma.cuh"
+#include "sweep_ckpt.cuh"
 #include "closures.cuh"
 
 namespace {
@@ -97,6 +98,7 @@ int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 
 struct DirData {
   DevBuf<rgfb::Coef3> c3;
+  DevBuf<double> c3s;  // SoA copy of c3 (y direction, checkpointed sweeps)
   DevBuf<double2> c1;
   DevBuf<double> idc;
   DevBuf<int64_t> seg_off;  // nlev*lines + 1
@@ -128,7 +130,10 @@ struct rgf_op {
   unsigned long long launches = 0;
   // streaming 3rd-RF path: bit-packed masks, closure classes and tables
   bool stream_ok = false;
+  bool ckpt_ok = true;  // checkpointed 3-pass sweeps (RGF_B200_TWOPASS=1: two-pass kernels)
+  DevBuf<double> ckpt;  // per-block causal checkpoints (apply scratch)
   DevBuf<uint64_t> bits[2];
+  DevBuf<uint64_t> bitsT[2];  // chain-minor copies (checkpointed sweeps)
   int64_t words[2] = {0, 0};
   DevBuf<int> cls_d;
   DevBuf<double> clos;  // [class][dir][nh][18]
@@ -182,8 +187,11 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.lev0 = lev0;
     a.nvar = nvar;
     a.c3 = d.c3.p;
+    a.c3s = d.c3s.p;
     a.idc = op->unit_dc ? d.idc.p : nullptr;
     a.bits = op->bits[dir].p;
+    a.bitsT = op->bitsT[dir].p;
+    a.nlev_all = op->nlev;
     a.words = op->words[dir];
     a.ghost = op->ghost_d.p;
     a.cls = op->cls_d.p;
@@ -198,6 +206,13 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.entry = op->entry.p;
     a.pre_scale = pre;
     a.post_scale = post;
+    if (op->ckpt_ok && rgfb::tma_supported(in, out, op->nx)) {
+      op->ckpt.alloc(static_cast<size_t>(std::max<int64_t>(1, rgfb::ckpt_doubles<T>(a))));
+      op->launches +=
+          static_cast<unsigned long long>(rgfb::launch_ckpt_sweep<T>(in, out, a, op->ckpt.p, st));
+      CUDA_OK(cudaGetLastError());
+      return;
+    }
     op->launches += static_cast<unsigned long long>(rgfb::launch_stream_sweep<T>(in, out, a, st));
     CUDA_OK(cudaGetLastError());
     return;
@@ -586,6 +601,20 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
         CUDA_OK(cudaDeviceSynchronize());
         op->stream_ok = true;
+        const char* tp = std::getenv("RGF_B200_TWOPASS");
+        op->ckpt_ok = !(tp && tp[0] == '1');
+        if (op->ckpt_ok) {
+          for (int dir = 0; dir < 2; ++dir) {
+            const int64_t tot = g->nlev * (dir == 0 ? g->ny : g->nx) * op->words[dir];
+            op->bitsT[dir].alloc(tot);
+            rgfb::k_bits_transpose<<<grid_for(tot, 256), 256>>>(
+                op->bits[dir].p, dir, g->nx, g->ny, g->nlev, op->words[dir], op->bitsT[dir].p);
+            CUDA_OK(cudaGetLastError());
+          }
+          op->dy_.c3s.alloc(static_cast<size_t>(4 * nh));
+          rgfb::k_coef_soa<<<grid_for(nh, 256), 256>>>(op->dy_.c3.p, g->nx, g->ny, op->dy_.c3s.p);
+          CUDA_OK(cudaGetLastError());
+        }
       }
     }
     if (opt->variance) {
@@ -659,10 +688,11 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
     uint64_t b = op->ghost_d.bytes() + op->variance.bytes() + op->in_d.bytes() +
                  op->pin[0].bytes() + op->pin[1].bytes() + op->pin[2].bytes() +
                  op->pout[0].bytes() + op->pout[1].bytes() + op->pout[2].bytes() +
-                 op->bits[0].bytes() + op->bits[1].bytes() + op->clos.bytes() + op->cls_d.bytes() + op->entry.bytes() +
+                 op->bits[0].bytes() + op->bits[1].bytes() + op->bitsT[0].bytes() +
+                 op->bitsT[1].bytes() + op->clos.bytes() + op->cls_d.bytes() + op->entry.bytes() +
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})
-      b += d->c3.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
+      b += d->c3.bytes() + d->c3s.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
            d->seg_line.bytes() + d->close_order.bytes();
     *out = b;
   });

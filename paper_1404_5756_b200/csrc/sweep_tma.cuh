@@ -167,12 +167,14 @@ struct AdjA2 {
 struct StageBits {
   int64_t wi = -1;
   uint64_t cur = 0, nxt = 0;
-  __device__ __forceinline__ void seek(const uint64_t* W, int64_t k, int64_t words, bool desc) {
+  // word i of the line at W[i * stride]
+  __device__ __forceinline__ void seek(const uint64_t* W, int64_t k, int64_t words, bool desc,
+                                       int64_t stride = 1) {
     const int64_t w = k >> 6;
     if (w == wi) return;
-    cur = (wi >= 0 && w == (desc ? wi - 1 : wi + 1)) ? nxt : ldw(W, w);
+    cur = (wi >= 0 && w == (desc ? wi - 1 : wi + 1)) ? nxt : ldw(W, w * stride);
     const int64_t wn = desc ? w - 1 : w + 1;
-    nxt = (wn >= 0 && wn < words) ? ldw(W, wn) : 0ull;
+    nxt = (wn >= 0 && wn < words) ? ldw(W, wn * stride) : 0ull;
     wi = w;
   }
   template <int U>
@@ -425,7 +427,6 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const int64_t iy = blockIdx.x / PB;
   const int64_t p0 = (blockIdx.x - iy * PB) * 32 * NW;
   const int npl = static_cast<int>(planes - p0 < 32 * NW ? planes - p0 : 32 * NW);
-  const int nwp = (npl + 31) / 32;
   constexpr bool need_idc = IDC;  // inv_dc table staged (fwd pass D / adjoint pass A)
   const int64_t nst = (n + U - 1) / U;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -335,3 +335,33 @@ def test_host_pipeline_matches_device_path(P, order, k, nx):
     want = gpu.apply(P.VT, g2.copy())
     gpu.apply(P.VT, g2, out=g2)  # in place through the pipeline
     assert np.array_equal(g2, want)
+
+
+def test_segment_ends_at_checkpoint_block_edges(P):
+    """Checkpointed sweeps cut lines into blocks (64 points in x, 32 rows in
+    y). Land cells are placed so segments end on a block's first, second and
+    last points and start on its first two, so the folded ghost entries owe
+    corrections to the block on the left."""
+    nx, ny, nlev = 200, 100, 5
+    g = uniform_grid(nx, ny, 5000.0, 6000.0, nlev=nlev)
+    mask = np.ones((nlev, ny, nx), dtype=bool)
+    xland = [[65], [66], [64], [62, 63], [1, 127, 130, 191]]
+    yland = [[33], [34], [32], [30, 31], [1, 63, 66, 95]]
+    for lev in range(nlev):
+        mask[lev][:, xland[lev]] = False
+        mask[lev][yland[lev], :] = False
+    g["mask"] = mask
+    rng = np.random.default_rng(77)
+    rx = g["dx"] * rng.uniform(1.5, 4.0, (ny, nx))
+    ry = g["dy"] * rng.uniform(1.5, 4.0, (ny, nx))
+    var = rng.uniform(0.5, 2.0, (nlev, ny, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
+    f = rng.standard_normal((2, nlev, ny, nx))
+    for name in KINDS:
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
+        assert np.all(got[:, ~mask] == 0.0)
+    got32 = gpu.apply(P.B, f.astype(np.float32))
+    want32 = cpu.apply(O.B, f.astype(np.float32).astype(np.float64))
+    assert relmax(got32, want32) <= TOL32
