@@ -52,6 +52,39 @@ __device__ __forceinline__ void restore(AdjA2& s, double r1, double r2, double r
   s.y32 = r2;
   s.y31 = r3;
 }
+// Segment-start reset as predicated zero moves (the compiler's selects cost
+// two FSEL per double on every step).
+__device__ __forceinline__ void zero_if(double& v, uint32_t on) {
+  asm("{\n .reg .pred p;\n setp.ne.u32 p, %1, 0;\n @p mov.f64 %0, 0d0000000000000000;\n}\n"
+      : "+d"(v)
+      : "r"(on));
+}
+__device__ __forceinline__ void reset_if(FwdA2& s, uint32_t on) {
+  zero_if(s.p1, on);
+  zero_if(s.p2, on);
+  zero_if(s.p3, on);
+}
+__device__ __forceinline__ void reset_if(AdjA2& s, uint32_t on) {
+  zero_if(s.u1, on);
+  zero_if(s.x1, on);
+  zero_if(s.y21, on);
+  zero_if(s.y22, on);
+  zero_if(s.y31, on);
+  zero_if(s.y32, on);
+  zero_if(s.y33, on);
+}
+// predicated streaming store (no branch around it)
+__device__ __forceinline__ void st_cs_if(double* p, double v, bool on) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.cs.f64 [%0], %1;\n}\n"
+               ::"l"(p), "d"(v), "r"(static_cast<uint32_t>(on))
+               : "memory");
+}
+__device__ __forceinline__ void st_cs_if(float* p, double v, bool on) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.global.cs.f32 [%0], %1;\n}\n"
+               ::"l"(p), "f"(static_cast<float>(v)), "r"(static_cast<uint32_t>(on))
+               : "memory");
+}
+
 // anti-causal entry states (as FwdD::enter / AdjD::enter)
 __device__ __forceinline__ void enter(FwdD2& s, const double3& e, const Coef3&) {
   s.q1 = e.x;
@@ -500,7 +533,7 @@ __global__ void __launch_bounds__(32 * R * NWR, 1)
 #pragma unroll
         for (int e = 0; e < EPC; ++e) {
           const int u = t * U + q * EPC + e;
-          if ((starts >> u) & 1u) sa.reset();
+          reset_if(sa, (starts >> u) & 1u);
           double w = v[e];
           if constexpr (TR && PRE) w *= __ldg(PREp + kb + u);
           if constexpr (TR && IDC) w *= id[u];
@@ -799,7 +832,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     double pv[X];
 #pragma unroll
     for (int u = 0; u < X; ++u) {
-      if ((starts >> u) & 1u) sa.reset();
+      reset_if(sa, (starts >> u) & 1u);
       double w = static_cast<double>(fld[u * 32]);
       if constexpr (TR && PRE) w *= __ldg(PREp + (kb + u) * nx);
       if constexpr (TR && IDC) w *= id[u * 32];
@@ -807,9 +840,9 @@ __global__ void __launch_bounds__(32 * NW, 1)
     }
 
     const int rvalid = act ? static_cast<int>(ny - kb < X ? ny - kb : X) : 0;
-    T* drow = dst + kb * nx;
+    T* dp = dst + (kb + X - 1) * nx;  // row u of the block, walked down by pointer
 #pragma unroll
-    for (int u = X - 1; u >= 0; --u) {
+    for (int u = X - 1; u >= 0; --u, dp -= nx) {
       const Coef3 c = cfu(u);
       if ((ends >> u) & 1u) {
         if (kb + u < ny - 1 && ghosts) {
@@ -825,7 +858,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
       double o = sd.step(c, c.b * pv[u]);
       if constexpr (!TR && IDC) o *= id[u * 32];
       if constexpr (POST) o *= __ldg(POSTp + (kb + u) * nx);
-      if (u < rvalid) __stcs(drow + u * nx, static_cast<T>(((sb >> u) & 1u) ? o : 0.0));
+      st_cs_if(dp, ((sb >> u) & 1u) ? o : 0.0, u < rvalid);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
