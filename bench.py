@@ -242,6 +242,20 @@ def main():
     n_rank = cfg.nx * cfg.ny * cfg.nlev * cfg.nvar
     value = n_rank * world / (ms * 1e-3) / 1e9
 
+    # final gather of the result into rank 0's field over NCCL (outside the
+    # timed region; levels need no other exchange)
+    gather = None
+    if world > 1:
+        from paper_1404_5756_b200.sharding import gather_levels
+        torch.cuda.synchronize()
+        dist.barrier()
+        g0 = time.perf_counter()
+        full = gather_levels(y, cfg.nlev * world)
+        torch.cuda.synchronize()
+        gather = {"ms": (time.perf_counter() - g0) * 1e3, "bytes": n_rank * w * world,
+                  "timing": "host wall clock, NCCL gather to rank 0 (not in value)"}
+        del full
+
     # per-kernel timing of the two directional sweeps (dominant kernel)
     sweep_ms = {}
     for name, kind in (("x", P.GX), ("y", P.GY)):
@@ -340,6 +354,8 @@ def main():
             "cpu_baseline": cpu,
             "build_seconds": build_s,
         }
+        if gather:
+            line["gather"] = gather
         if extra:
             line["extra"] = extra
         print(json.dumps(line), flush=True)

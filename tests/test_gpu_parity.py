@@ -365,3 +365,23 @@ def test_segment_ends_at_checkpoint_block_edges(P):
     got32 = gpu.apply(P.B, f.astype(np.float32))
     want32 = cpu.apply(O.B, f.astype(np.float32).astype(np.float64))
     assert relmax(got32, want32) <= TOL32
+
+
+def test_level_sharded_ops_match_full_op(P):
+    """Per-rank operators over level blocks (paper_1404_5756_b200.sharding),
+    run here one after the other on one GPU, reproduce the full operator bit
+    for bit: a level's result does not depend on the other levels."""
+    from paper_1404_5756_b200.sharding import ShardedCovarianceOp
+    g, rx, ry = random_case(404, nx=64, ny=40, nlev=7, sea=0.7)
+    var = np.random.default_rng(9).uniform(0.5, 2.0, (7, 40, 64))
+    f = np.random.default_rng(10).standard_normal((2, 7, 40, 64))
+    full, _ = build_pair(P, g, rx, ry, variance=var)
+    for name in ("GYGX", "B"):
+        want = full.apply(getattr(P, name), f)
+        parts = []
+        for r in range(3):
+            sop = ShardedCovarianceOp(64, 40, g["dx"], g["dy"], g["mask"], rx, ry,
+                                      P.CovarianceOptions(), nlev=7, world=3, rank=r,
+                                      variance=var)
+            parts.append(sop.apply(getattr(P, name), np.ascontiguousarray(sop.local_slice(f))))
+        assert np.array_equal(np.concatenate(parts, axis=1), want), name
