@@ -721,23 +721,26 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   }
 }
 
-template <typename T, int NW>
+template <typename T, int NPL>
 struct YC2 {
   static constexpr int X = kCkY;
-  static constexpr size_t field = size_t(NW) * X * 32 * sizeof(T);
+  static constexpr size_t field = size_t(NPL) * X * 32 * sizeof(T);
   static constexpr size_t coef = size_t(X) * 4 * 32 * sizeof(double);
   static constexpr size_t idc = size_t(X) * 32 * sizeof(double);
   static constexpr size_t bytes = (field + coef + idc + 1023) / 1024 * 1024;
 };
 
-// C2, y: blocks of X rows, descending; lanes = columns, warps = planes;
-// results go straight to global memory (coalesced 32-column rows).
-template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int S>
+// C2, y: blocks of X rows, descending; lanes = columns, each warp carries PPW
+// planes (independent chains interleaved: ILP, and one coefficient load
+// serves PPW chains); results go straight to global memory (coalesced
+// 32-column rows).
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_yck2(T* __restrict__ out, StreamArgs a, const double* __restrict__ ck,
            const __grid_constant__ CUtensorMap tm_field, const __grid_constant__ CUtensorMap tm_coef,
            const __grid_constant__ CUtensorMap tm_idc) {
-  using L = YC2<T, NW>;
+  constexpr int NPL = NW * PPW;  // planes per CTA
+  using L = YC2<T, NPL>;
   constexpr int X = L::X;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
@@ -746,12 +749,13 @@ __global__ void __launch_bounds__(32 * NW, 1)
 
   const int64_t nx = a.nx, ny = a.ny, nh = nx * ny;
   const int64_t planes = a.nvar * a.nlev;
-  const int64_t PB = (planes + NW - 1) / NW;
+  const int64_t PB = (planes + NPL - 1) / NPL;
   const int64_t tile = blockIdx.x / PB;
-  const int64_t p0 = (blockIdx.x - tile * PB) * NW;
+  const int64_t p0 = (blockIdx.x - tile * PB) * NPL;
   const int64_t ix0 = tile * 32;
   const int ncol = static_cast<int>(nx - ix0 < 32 ? nx - ix0 : 32);
-  const int nwp = static_cast<int>(planes - p0 < NW ? planes - p0 : NW);
+  const int npl = static_cast<int>(planes - p0 < NPL ? planes - p0 : NPL);
+  const int nwp = (npl + PPW - 1) / PPW;
   const int64_t NB = (ny + X - 1) / X;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -784,23 +788,38 @@ __global__ void __launch_bounds__(32 * NW, 1)
   __syncthreads();
   if (warp >= nwp) return;
 
-  const int64_t p = p0 + warp;
-  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
-  (void)var;
-  const bool act = lane < ncol;
-  const int64_t ix = ix0 + (act ? lane : 0);
-  T* dst = out + p * nh + ix;
-  const uint64_t* W = a.bitsT + lev * a.words * nx + ix;
-  const double* PREp = PRE ? a.pre_scale + lev * nh + ix : nullptr;
-  const double* POSTp = POST ? a.post_scale + lev * nh + ix : nullptr;
-  const double* Mcol = a.clos + clos_off(a.cls[lev], 1, TR ? 1 : 0, nh, ix);
-  const bool ghosts = a.ghost[lev] > 0;
-  typename std::conditional<TR, AdjA2, FwdA2>::type sa;
-  typename std::conditional<TR, AdjD2, FwdD2>::type sd;
-  auto meta = [&](int64_t b) {
-    return load_meta<X>(ck + ((p * NB + b) * 3) * nx + ix, b > 0, nx, W, nx, b * X, a.words);
+  const bool colok = lane < ncol;
+  const int64_t ix = ix0 + (colok ? lane : 0);
+  T* dst[PPW];
+  const uint64_t* W[PPW];
+  const double* PREp[PPW];
+  const double* POSTp[PPW];
+  const double* Mcol[PPW];
+  bool ghosts[PPW], act[PPW];
+  int64_t pp[PPW];
+#pragma unroll
+  for (int c = 0; c < PPW; ++c) {
+    const int pl = warp * PPW + c;
+    act[c] = colok && pl < npl;
+    const int64_t p = p0 + (pl < npl ? pl : 0);
+    pp[c] = p;
+    const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
+    dst[c] = out + p * nh + ix;
+    W[c] = a.bitsT + lev * a.words * nx + ix;
+    PREp[c] = PRE ? a.pre_scale + lev * nh + ix : nullptr;
+    POSTp[c] = POST ? a.post_scale + lev * nh + ix : nullptr;
+    Mcol[c] = a.clos + clos_off(a.cls[lev], 1, TR ? 1 : 0, nh, ix);
+    ghosts[c] = a.ghost[lev] > 0;
+  }
+  typename std::conditional<TR, AdjA2, FwdA2>::type sa[PPW];
+  typename std::conditional<TR, AdjD2, FwdD2>::type sd[PPW];
+  auto meta = [&](int c, int64_t b) {
+    return load_meta<X>(ck + ((pp[c] * NB + b) * 3) * nx + ix, b > 0 && act[c], nx, W[c], nx,
+                        b * X, a.words);
   };
-  BlockMeta next = meta(NB - 1);
+  BlockMeta next[PPW];
+#pragma unroll
+  for (int c = 0; c < PPW; ++c) next[c] = meta(c, NB - 1);
 
   for (int64_t bi = 0; bi < NB; ++bi) {
     const int s = static_cast<int>(bi % S);
@@ -810,55 +829,82 @@ __global__ void __launch_bounds__(32 * NW, 1)
       mbar_wait(&empty[(bi - 1) % S], static_cast<uint32_t>(((bi - 1) / S) & 1));
       load_block(bi - 1 + S);
     }
-    const BlockMeta cur = next;
-    if (b > 0) next = meta(b - 1);  // consumed one block from now
-    const double r1 = cur.r1, r2 = cur.r2, r3 = cur.r3;
-    const BlockBits bb = decode_bits<X>(cur, kb, a.words);
-    const uint32_t sb = bb.sb, sm1 = bb.sm1, sm2 = bb.sm2, after = bb.after;
-    const uint32_t starts = sb & ~((sb << 1) | sm1);
-    const uint32_t ends = sb & ~((sb >> 1) | (after << (X - 1)));
-    const int jl = first_end(ends);
-    Closure mpre{};
-    mpre = prefetch_closure(Mcol + (kb + (jl > 0 ? jl : 0)) * nx * 10,
-                            jl >= 0 && kb + jl < ny - 1 && ghosts);
+    double r1[PPW], r2[PPW], r3[PPW];
+    uint32_t sb[PPW], sm1[PPW], sm2[PPW], starts[PPW], ends[PPW];
+    int jl[PPW];
+    Closure mpre[PPW];
+#pragma unroll
+    for (int c = 0; c < PPW; ++c) {
+      const BlockMeta cur = next[c];
+      if (b > 0) next[c] = meta(c, b - 1);  // consumed one block from now
+      r1[c] = cur.r1;
+      r2[c] = cur.r2;
+      r3[c] = cur.r3;
+      const BlockBits bb = decode_bits<X>(cur, kb, a.words);
+      sb[c] = bb.sb;
+      sm1[c] = bb.sm1;
+      sm2[c] = bb.sm2;
+      starts[c] = bb.sb & ~((bb.sb << 1) | bb.sm1);
+      ends[c] = bb.sb & ~((bb.sb >> 1) | (bb.after << (X - 1)));
+      jl[c] = first_end(ends[c]);
+      mpre[c] = prefetch_closure(Mcol[c] + (kb + (jl[c] > 0 ? jl[c] : 0)) * nx * 10,
+                                 jl[c] >= 0 && kb + jl[c] < ny - 1 && ghosts[c]);
+    }
     mbar_wait(&full[s], static_cast<uint32_t>((bi / S) & 1));
     const unsigned char* base = smem + s * L::bytes;
-    const T* fld = reinterpret_cast<const T*>(base) + warp * X * 32 + lane;
+    const T* fld = reinterpret_cast<const T*>(base) + warp * PPW * X * 32 + lane;
     const double* cs = reinterpret_cast<const double*>(base + L::field);
     const double* id = reinterpret_cast<const double*>(base + L::field + L::coef) + lane;
     auto cfu = [&](int uu) -> Coef3 { return coef_soa<X>(cs, uu, lane); };
 
-    restore(sa, r1, r2, r3);
-    double pv[X];
+#pragma unroll
+    for (int c = 0; c < PPW; ++c) restore(sa[c], r1[c], r2[c], r3[c]);
+    double pv[PPW][X];
 #pragma unroll
     for (int u = 0; u < X; ++u) {
-      reset_if(sa, (starts >> u) & 1u);
-      double w = static_cast<double>(fld[u * 32]);
-      if constexpr (TR && PRE) w *= __ldg(PREp + (kb + u) * nx);
-      if constexpr (TR && IDC) w *= id[u * 32];
-      pv[u] = sa.step(cfu(u), w);
+      const Coef3 cu = cfu(u);
+      double idu = 1.0;
+      if constexpr (TR && IDC) idu = id[u * 32];
+#pragma unroll
+      for (int c = 0; c < PPW; ++c) {
+        reset_if(sa[c], (starts[c] >> u) & 1u);
+        double w = static_cast<double>(fld[(c * X + u) * 32]);
+        if constexpr (TR && PRE) w *= __ldg(PREp[c] + (kb + u) * nx);
+        if constexpr (TR && IDC) w *= idu;
+        pv[c][u] = sa[c].step(cu, w);
+      }
     }
 
-    const int rvalid = act ? static_cast<int>(ny - kb < X ? ny - kb : X) : 0;
-    T* dp = dst + (kb + X - 1) * nx;  // row u of the block, walked down by pointer
+    const int rvalid = colok ? static_cast<int>(ny - kb < X ? ny - kb : X) : 0;
+    T* dp[PPW];
 #pragma unroll
-    for (int u = X - 1; u >= 0; --u, dp -= nx) {
-      const Coef3 c = cfu(u);
-      if ((ends >> u) & 1u) {
-        if (kb + u < ny - 1 && ghosts) {
-          const bool s1 = u >= 1 ? ((sb >> (u >= 1 ? u - 1 : 0)) & 1u) : sm1;
-          const bool s2 =
-              s1 && (u >= 2 ? ((sb >> (u >= 2 ? u - 2 : 0)) & 1u) : (u == 1 ? sm1 : sm2));
-          const Closure M = u == jl ? mpre : load_closure(Mcol + (kb + u) * nx * 10);
-          enter(sd, segment_entry<TR, X>(pv, u, r1, r2, r3, s1, s2, c, cfu, M), c);
-        } else {
-          sd.reset();
+    for (int c = 0; c < PPW; ++c) dp[c] = dst[c] + (kb + X - 1) * nx;  // walked down by pointer
+#pragma unroll
+    for (int u = X - 1; u >= 0; --u) {
+      const Coef3 cu = cfu(u);
+      double idu = 1.0;
+      if constexpr (!TR && IDC) idu = id[u * 32];
+#pragma unroll
+      for (int c = 0; c < PPW; ++c) {
+        if ((ends[c] >> u) & 1u) {
+          if (kb + u < ny - 1 && ghosts[c]) {
+            const bool s1 = u >= 1 ? ((sb[c] >> (u >= 1 ? u - 1 : 0)) & 1u) : sm1[c];
+            const bool s2 = s1 && (u >= 2 ? ((sb[c] >> (u >= 2 ? u - 2 : 0)) & 1u)
+                                          : (u == 1 ? sm1[c] : sm2[c]));
+            const Closure M =
+                u == jl[c] ? mpre[c] : load_closure(Mcol[c] + (kb + u) * nx * 10);
+            enter(sd[c], segment_entry<TR, X>(pv[c], u, r1[c], r2[c], r3[c], s1, s2, cu, cfu, M),
+                  cu);
+          } else {
+            sd[c].reset();
+          }
         }
+        double o = sd[c].step(cu, cu.b * pv[c][u]);
+        if constexpr (!TR && IDC) o *= idu;
+        if constexpr (POST) o *= __ldg(POSTp[c] + (kb + u) * nx);
+        st_cs_if(dp[c], ((sb[c] >> u) & 1u) ? o : 0.0, act[c] && u < rvalid);
+        dp[c] -= nx;
       }
-      double o = sd.step(c, c.b * pv[u]);
-      if constexpr (!TR && IDC) o *= id[u * 32];
-      if constexpr (POST) o *= __ldg(POSTp + (kb + u) * nx);
-      st_cs_if(dp, ((sb >> u) & 1u) ? o : 0.0, u < rvalid);
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[s]);
@@ -866,7 +912,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
 }
 
 constexpr int kYc1NW = 16, kYc1U = 8, kYc1S = 4;
-constexpr int kYc2NW = 16, kYc2S = 2;
+constexpr int kYc2NW = 16, kYc2PPW = 1, kYc2S = 2;
 constexpr int kXc1NW = 4, kXc1S = 4;
 constexpr int kXc2R = 4, kXc2NWR = 4, kXc2S = 3;
 
@@ -989,12 +1035,12 @@ void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
 
 template <typename T, bool TR, bool IDC, bool PRE, bool POST>
 void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
-  constexpr int NW = kYc2NW, S = kYc2S;
-  using L = YC2<T, NW>;
+  constexpr int NW = kYc2NW, PPW = kYc2PPW, S = kYc2S, NPL = NW * PPW;
+  using L = YC2<T, NPL>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_yck2<T, TR, IDC, PRE, POST, NW, S>,
+    cudaFuncSetAttribute(k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
@@ -1002,7 +1048,7 @@ void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cud
   const uint64_t sz = sizeof(T);
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
   const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
-  const uint32_t fb[3] = {32, uint32_t(L::X), uint32_t(NW)};
+  const uint32_t fb[3] = {32, uint32_t(L::X), uint32_t(NPL)};
   const CUtensorMap tf = make_tmap(in, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tc = coef_soa_map(a, L::X);
   const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
@@ -1011,8 +1057,9 @@ void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cud
   const CUtensorMap ti = IDC ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
                                          CU_TENSOR_MAP_SWIZZLE_NONE)
                              : tc;
-  const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NW - 1) / NW);
-  k_yck2<T, TR, IDC, PRE, POST, NW, S><<<blocks, 32 * NW, smem, st>>>(out, a, ck, tf, tc, ti);
+  const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NPL - 1) / NPL);
+  k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S><<<blocks, 32 * NW, smem, st>>>(out, a, ck, tf, tc,
+                                                                          ti);
 }
 
 // runtime flags -> template flags; returns kernel launches
