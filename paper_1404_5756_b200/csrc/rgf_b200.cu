@@ -99,6 +99,7 @@ int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
 struct DirData {
   DevBuf<rgfb::Coef3> c3;
   DevBuf<double> c3s;  // SoA copy of c3 (y direction, checkpointed sweeps)
+  DevBuf<double> idcp;  // inv_dc with even row pitch when nx is odd (TMA)
   DevBuf<double2> c1;
   DevBuf<double> idc;
   DevBuf<int64_t> seg_off;  // nlev*lines + 1
@@ -144,6 +145,7 @@ struct rgf_op {
   cudaEvent_t pipe_ev[3][3] = {};
   cudaEvent_t pipe_ev_user = nullptr;
   DevBuf<char> pin[3], pout[3];
+  DevBuf<char> pdin, pdout;  // pitched copies for device applies on unaligned rows
   void pipe_init() {
     if (pipe_stream[0]) return;
     for (auto& s : pipe_stream) CUDA_OK(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking));
@@ -170,9 +172,21 @@ namespace {
 // One directional sweep over every (var, level, line): out = G_dir in (or
 // its transpose), with optional fused per-point input/output scaling
 // (the variance multiplies of apply_v / apply_v_transpose).
+// Field row pitch (elements) the checkpointed kernels run on: nx, or nx
+// rounded up to a 16 B multiple when the dense rows are not TMA-aligned
+// (SURVEY §7 hard part 4: C2 fp64 nx=871, C4 fp32 nx=1442). Other kernels
+// always use the dense layout.
+template <typename T>
+int64_t field_pitch(const rgf_op* op) {
+  if (!op->stream_ok || !op->ckpt_ok) return op->nx;
+  const int64_t q = 16 / static_cast<int64_t>(sizeof(T));
+  return (op->nx + q - 1) / q * q;
+}
+
 template <typename T>
 void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nvar,
-           int64_t lev0, int64_t nlev, const double* pre, const double* post, cudaStream_t st) {
+           int64_t lev0, int64_t nlev, const double* pre, const double* post, cudaStream_t st,
+           int64_t pitch) {
   const DirData& d = dir == 0 ? op->dx_ : op->dy_;
   const int64_t lines = nvar * nlev * (dir == 0 ? op->ny : op->nx);
 
@@ -183,12 +197,15 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.unit_dc = op->unit_dc;
     a.nx = op->nx;
     a.ny = op->ny;
+    a.pitch = pitch;
     a.nlev = nlev;
     a.lev0 = lev0;
     a.nvar = nvar;
     a.c3 = d.c3.p;
     a.c3s = d.c3s.p;
     a.idc = op->unit_dc ? d.idc.p : nullptr;
+    a.ipitch = (op->nx + 1) / 2 * 2;
+    a.idcp = !op->unit_dc ? nullptr : (a.ipitch == op->nx ? d.idc.p : d.idcp.p);
     a.bits = op->bits[dir].p;
     a.bitsT = op->bitsT[dir].p;
     a.nlev_all = op->nlev;
@@ -206,17 +223,19 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.entry = op->entry.p;
     a.pre_scale = pre;
     a.post_scale = post;
-    if (op->ckpt_ok && rgfb::tma_supported(in, out, op->nx)) {
+    if (op->ckpt_ok && rgfb::tma_supported(in, out, pitch)) {
       op->ckpt.alloc(static_cast<size_t>(std::max<int64_t>(1, rgfb::ckpt_doubles<T>(a))));
       op->launches +=
           static_cast<unsigned long long>(rgfb::launch_ckpt_sweep<T>(in, out, a, op->ckpt.p, st));
       CUDA_OK(cudaGetLastError());
       return;
     }
+    if (pitch != op->nx) throw std::runtime_error("sweep: pitched field on a dense-only path");
     op->launches += static_cast<unsigned long long>(rgfb::launch_stream_sweep<T>(in, out, a, st));
     CUDA_OK(cudaGetLastError());
     return;
   }
+  if (pitch != op->nx) throw std::runtime_error("sweep: pitched field on a dense-only path");
 
   const int64_t n = dir == 0 ? op->nx : op->ny;
   const int64_t slab = n + 2 * op->gmax + 4;
@@ -256,15 +275,15 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
 
 template <typename T>
 void apply_typed(rgf_op* op, int kind, const T* in, T* out, int64_t nvar, int64_t lev0,
-                 int64_t nlev, cudaStream_t st) {
-  const size_t count = static_cast<size_t>(nvar * nlev * op->nx * op->ny);
+                 int64_t nlev, cudaStream_t st, int64_t pitch) {
+  const size_t count = static_cast<size_t>(nvar * nlev * pitch * op->ny);
   const double* var = op->has_variance ? op->variance.p : nullptr;
   auto tmp = [&](DevBuf<char>& b) {
     b.alloc(count * sizeof(T));
     return reinterpret_cast<T*>(b.p);
   };
   auto sw = [&](int dir, bool tr, const T* i, T* o, const double* pre, const double* post) {
-    sweep<T>(op, dir, tr, i, o, nvar, lev0, nlev, pre, post, st);
+    sweep<T>(op, dir, tr, i, o, nvar, lev0, nlev, pre, post, st, pitch);
   };
   switch (kind) {
     case RGF_GX: sw(0, false, in, out, nullptr, nullptr); break;
@@ -321,7 +340,10 @@ void apply_host_pipelined(rgf_op* op, int kind, const T* hin, T* hout, int64_t n
   cl = std::min(cl, nlev);
   constexpr int kSlots = 3;
   op->pipe_init();
-  const size_t slot_bytes = static_cast<size_t>(cl * nh) * sizeof(T);
+  // device slots use the kernels' row pitch; 2-D copies repack on the fly
+  const int64_t pitch = field_pitch<T>(op);
+  const size_t esz = sizeof(T);
+  const size_t slot_bytes = static_cast<size_t>(cl * op->ny * pitch) * esz;
   for (int sl = 0; sl < kSlots; ++sl) {
     op->pin[sl].alloc(slot_bytes);
     op->pout[sl].alloc(slot_bytes);
@@ -337,24 +359,49 @@ void apply_host_pipelined(rgf_op* op, int kind, const T* hin, T* hout, int64_t n
       const int64_t nl = std::min(cl, nlev - l0);
       const int sl = static_cast<int>(c % kSlots);
       const size_t off = static_cast<size_t>((v * nlev + l0) * nh);
-      const size_t bytes = static_cast<size_t>(nl * nh) * sizeof(T);
+      const size_t rows = static_cast<size_t>(nl * op->ny);
       T* din = reinterpret_cast<T*>(op->pin[sl].p);
       T* dout = reinterpret_cast<T*>(op->pout[sl].p);
       cudaEvent_t* ev = op->pipe_ev[sl];  // 0: loaded, 1: computed, 2: drained
       // slot reuse: din is free once the chunk kSlots back was computed,
       // dout once it was drained
       if (c >= kSlots) CUDA_OK(cudaStreamWaitEvent(h2d, ev[1], 0));
-      CUDA_OK(cudaMemcpyAsync(din, hin + off, bytes, cudaMemcpyHostToDevice, h2d));
+      CUDA_OK(cudaMemcpy2DAsync(din, pitch * esz, hin + off, op->nx * esz, op->nx * esz, rows,
+                                cudaMemcpyHostToDevice, h2d));
       CUDA_OK(cudaEventRecord(ev[0], h2d));
       CUDA_OK(cudaStreamWaitEvent(cs, ev[0], 0));
       if (c >= kSlots) CUDA_OK(cudaStreamWaitEvent(cs, ev[2], 0));
-      apply_typed<T>(op, kind, din, dout, 1, l0, nl, cs);
+      apply_typed<T>(op, kind, din, dout, 1, l0, nl, cs, pitch);
       CUDA_OK(cudaEventRecord(ev[1], cs));
       CUDA_OK(cudaStreamWaitEvent(d2h, ev[1], 0));
-      CUDA_OK(cudaMemcpyAsync(hout + off, dout, bytes, cudaMemcpyDeviceToHost, d2h));
+      CUDA_OK(cudaMemcpy2DAsync(hout + off, op->nx * esz, dout, pitch * esz, op->nx * esz, rows,
+                                cudaMemcpyDeviceToHost, d2h));
       CUDA_OK(cudaEventRecord(ev[2], d2h));
     }
   CUDA_OK(cudaStreamSynchronize(d2h));
+}
+
+// Device-memory apply. Dense rows that are not 16 B aligned go through
+// internal pitched buffers (one 2-D copy each way) so the checkpointed TMA
+// kernels still run.
+template <typename T>
+void apply_device(rgf_op* op, int kind, const T* in, T* out, int64_t nvar, cudaStream_t st) {
+  const int64_t pitch = field_pitch<T>(op);
+  if (pitch == op->nx) {
+    apply_typed<T>(op, kind, in, out, nvar, 0, op->nlev, st, pitch);
+    return;
+  }
+  const size_t esz = sizeof(T);
+  const size_t rows = static_cast<size_t>(nvar * op->nlev * op->ny);
+  op->pdin.alloc(rows * pitch * esz);
+  op->pdout.alloc(rows * pitch * esz);
+  T* din = reinterpret_cast<T*>(op->pdin.p);
+  T* dout = reinterpret_cast<T*>(op->pdout.p);
+  CUDA_OK(cudaMemcpy2DAsync(din, pitch * esz, in, op->nx * esz, op->nx * esz, rows,
+                            cudaMemcpyDeviceToDevice, st));
+  apply_typed<T>(op, kind, din, dout, nvar, 0, op->nlev, st, pitch);
+  CUDA_OK(cudaMemcpy2DAsync(out, op->nx * esz, dout, pitch * esz, op->nx * esz, rows,
+                            cudaMemcpyDeviceToDevice, st));
 }
 
 unsigned long long read_u64(const unsigned long long* d) {
@@ -611,6 +658,14 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
                 op->bits[dir].p, dir, g->nx, g->ny, g->nlev, op->words[dir], op->bitsT[dir].p);
             CUDA_OK(cudaGetLastError());
           }
+          if (op->unit_dc && (g->nx & 1)) {  // even-pitch inv_dc copies for the TMA maps
+            const int64_t ip = g->nx + 1;
+            for (DirData* dd : {&op->dx_, &op->dy_}) {
+              dd->idcp.alloc(static_cast<size_t>(ip * g->ny));
+              CUDA_OK(cudaMemcpy2D(dd->idcp.p, ip * 8, dd->idc.p, g->nx * 8, g->nx * 8, g->ny,
+                                   cudaMemcpyDeviceToDevice));
+            }
+          }
           op->dy_.c3s.alloc(static_cast<size_t>(4 * nh));
           rgfb::k_coef_soa<<<grid_for(nh, 256), 256>>>(op->dy_.c3.p, g->nx, g->ny, op->dy_.c3s.p);
           CUDA_OK(cudaGetLastError());
@@ -658,11 +713,11 @@ int rgf_op_apply(rgf_op* op, int kind, int dtype, const void* in, void* out, int
     }
     if (memory != RGF_DEVICE) throw InvalidArgument("apply: unknown memory kind");
     if (dtype == RGF_F64)
-      apply_typed<double>(op, kind, static_cast<const double*>(in), static_cast<double*>(out),
-                          nvar, 0, op->nlev, st);
+      apply_device<double>(op, kind, static_cast<const double*>(in), static_cast<double*>(out),
+                           nvar, st);
     else
-      apply_typed<float>(op, kind, static_cast<const float*>(in), static_cast<float*>(out), nvar,
-                         0, op->nlev, st);
+      apply_device<float>(op, kind, static_cast<const float*>(in), static_cast<float*>(out), nvar,
+                          st);
   });
 }
 
@@ -687,12 +742,13 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
     if (!op || !out) throw InvalidArgument("device_bytes: null argument");
     uint64_t b = op->ghost_d.bytes() + op->variance.bytes() + op->in_d.bytes() +
                  op->pin[0].bytes() + op->pin[1].bytes() + op->pin[2].bytes() +
+                 op->pdin.bytes() + op->pdout.bytes() +
                  op->pout[0].bytes() + op->pout[1].bytes() + op->pout[2].bytes() +
                  op->bits[0].bytes() + op->bits[1].bytes() + op->bitsT[0].bytes() +
                  op->bitsT[1].bytes() + op->clos.bytes() + op->cls_d.bytes() + op->entry.bytes() +
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})
-      b += d->c3.bytes() + d->c3s.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
+      b += d->c3.bytes() + d->c3s.bytes() + d->idcp.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
            d->seg_line.bytes() + d->close_order.bytes();
     *out = b;
   });

@@ -804,7 +804,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     const int64_t p = p0 + (pl < npl ? pl : 0);
     pp[c] = p;
     const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
-    dst[c] = out + p * nh + ix;
+    dst[c] = out + p * a.pitch * ny + ix;  // field rows are `pitch` apart
     W[c] = a.bitsT + lev * a.words * nx + ix;
     PREp[c] = PRE ? a.pre_scale + lev * nh + ix : nullptr;
     POSTp[c] = POST ? a.post_scale + lev * nh + ix : nullptr;
@@ -878,7 +878,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
     const int rvalid = colok ? static_cast<int>(ny - kb < X ? ny - kb : X) : 0;
     T* dp[PPW];
 #pragma unroll
-    for (int c = 0; c < PPW; ++c) dp[c] = dst[c] + (kb + X - 1) * nx;  // walked down by pointer
+    for (int c = 0; c < PPW; ++c) dp[c] = dst[c] + (kb + X - 1) * a.pitch;  // walked down
 #pragma unroll
     for (int u = X - 1; u >= 0; --u) {
       const Coef3 cu = cfu(u);
@@ -903,7 +903,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
         if constexpr (!TR && IDC) o *= idu;
         if constexpr (POST) o *= __ldg(POSTp[c] + (kb + u) * nx);
         st_cs_if(dp[c], ((sb[c] >> u) & 1u) ? o : 0.0, act[c] && u < rvalid);
-        dp[c] -= nx;
+        dp[c] -= a.pitch;
       }
     }
     __syncwarp();
@@ -938,7 +938,7 @@ void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
   const int64_t planes = a.nvar * a.nlev;
   const uint64_t sz = sizeof(T);
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
-  const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
+  const uint64_t fs[2] = {uint64_t(a.pitch) * sz, uint64_t(a.pitch * a.ny) * sz};
   const uint32_t fb[3] = {uint32_t(L::U), 1, uint32_t(32 * NW)};
   const CUtensorMap tin = make_tmap(in, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
@@ -948,9 +948,9 @@ void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
   const CUtensorMap tc =
       make_tmap(a.c3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb, CU_TENSOR_MAP_SWIZZLE_NONE);
   const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
-  const uint64_t is[1] = {uint64_t(a.nx) * 8};
+  const uint64_t is[1] = {uint64_t(a.ipitch) * 8};  // TMA: 16 B multiple
   const uint32_t ib[2] = {uint32_t(L::U), 1};
-  const CUtensorMap ti = IDC ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+  const CUtensorMap ti = IDC ? make_tmap(a.idcp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
                                          CU_TENSOR_MAP_SWIZZLE_NONE)
                              : tc;
   const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
@@ -972,7 +972,7 @@ void launch_xck2(const T* in, T* out, const StreamArgs& a, const double* ck, cud
   const uint64_t sz = sizeof(T);
   // dims (x, plane, row): box rows land in smem as [row][plane][x]
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(planes), uint64_t(a.ny)};
-  const uint64_t fs[2] = {uint64_t(a.nx * a.ny) * sz, uint64_t(a.nx) * sz};
+  const uint64_t fs[2] = {uint64_t(a.pitch * a.ny) * sz, uint64_t(a.pitch) * sz};
   const uint32_t fb[3] = {uint32_t(L::U), uint32_t(32 * NWR), uint32_t(R)};
   const CUtensorMap tin = make_tmap(in, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B,
                                     CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
@@ -985,9 +985,9 @@ void launch_xck2(const T* in, T* out, const StreamArgs& a, const double* ck, cud
   const CUtensorMap tc =
       make_tmap(a.c3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb, CU_TENSOR_MAP_SWIZZLE_NONE);
   const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
-  const uint64_t is[1] = {uint64_t(a.nx) * 8};
+  const uint64_t is[1] = {uint64_t(a.ipitch) * 8};  // TMA: 16 B multiple
   const uint32_t ib[2] = {uint32_t(L::X), uint32_t(R)};
-  const CUtensorMap ti = IDC ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+  const CUtensorMap ti = IDC ? make_tmap(a.idcp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
                                          CU_TENSOR_MAP_SWIZZLE_NONE)
                              : tc;
   const int64_t PB = (planes + 32 * NWR - 1) / (32 * NWR);
@@ -1019,14 +1019,14 @@ void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
   const int64_t planes = a.nvar * a.nlev;
   const uint64_t sz = sizeof(T);
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
-  const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
+  const uint64_t fs[2] = {uint64_t(a.pitch) * sz, uint64_t(a.pitch * a.ny) * sz};
   const uint32_t fb[3] = {32, uint32_t(U), uint32_t(NW)};
   const CUtensorMap tf = make_tmap(in, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tc = coef_soa_map(a, U);
   const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
-  const uint64_t is[1] = {uint64_t(a.nx) * 8};
+  const uint64_t is[1] = {uint64_t(a.ipitch) * 8};  // TMA: 16 B multiple
   const uint32_t ib[2] = {32, uint32_t(U)};
-  const CUtensorMap ti = IDC ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+  const CUtensorMap ti = IDC ? make_tmap(a.idcp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
                                          CU_TENSOR_MAP_SWIZZLE_NONE)
                              : tc;
   const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NW - 1) / NW);
@@ -1047,14 +1047,14 @@ void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cud
   const int64_t planes = a.nvar * a.nlev;
   const uint64_t sz = sizeof(T);
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
-  const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
+  const uint64_t fs[2] = {uint64_t(a.pitch) * sz, uint64_t(a.pitch * a.ny) * sz};
   const uint32_t fb[3] = {32, uint32_t(L::X), uint32_t(NPL)};
   const CUtensorMap tf = make_tmap(in, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tc = coef_soa_map(a, L::X);
   const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
-  const uint64_t is[1] = {uint64_t(a.nx) * 8};
+  const uint64_t is[1] = {uint64_t(a.ipitch) * 8};  // TMA: 16 B multiple
   const uint32_t ib[2] = {32, uint32_t(L::X)};
-  const CUtensorMap ti = IDC ? make_tmap(a.idc, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+  const CUtensorMap ti = IDC ? make_tmap(a.idcp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
                                          CU_TENSOR_MAP_SWIZZLE_NONE)
                              : tc;
   const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NPL - 1) / NPL);

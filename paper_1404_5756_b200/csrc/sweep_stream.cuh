@@ -47,11 +47,14 @@ namespace rgfb {
 struct StreamArgs {
   int dir, transpose, unit_dc;
   int64_t nx, ny, nlev, nvar;
+  int64_t pitch;            // field row stride in elements (>= nx; checkpointed kernels)
   int64_t lev0;             // first global level of this launch
   int64_t nlev_all;         // levels of the operator (bitsT stride)
   const Coef3* c3;
   const double* c3s;        // y direction only: SoA rows [ny][4][nx] (checkpointed sweeps)
   const double* idc;
+  const double* idcp;       // idc with rows `ipitch` apart (16 B multiple; TMA maps)
+  int64_t ipitch;
   const uint64_t* bits;     // bit-packed masks for this direction
   const uint64_t* bitsT;    // same words, chain-minor: x [iy][word][lev], y [lev][word][ix]
   int64_t words;            // 64-bit words per line

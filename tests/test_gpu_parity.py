@@ -385,3 +385,40 @@ def test_level_sharded_ops_match_full_op(P):
                                       variance=var)
             parts.append(sop.apply(getattr(P, name), np.ascontiguousarray(sop.local_slice(f))))
         assert np.array_equal(np.concatenate(parts, axis=1), want), name
+
+
+@pytest.mark.parametrize("nx", [57, 96])
+def test_two_pass_kernels_still_match(P, monkeypatch, nx):
+    """RGF_B200_TWOPASS=1 keeps the two-pass kernels (TMA pass A/D for
+    aligned rows, the register/cp.async kernels for unaligned rows)."""
+    g, rx, ry = random_case(515 + nx, nx=nx, ny=37, nlev=3)
+    var = np.random.default_rng(13).uniform(0.5, 2.0, (3, 37, nx))
+    monkeypatch.setenv("RGF_B200_TWOPASS", "1")
+    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
+    monkeypatch.delenv("RGF_B200_TWOPASS")
+    f = np.random.default_rng(14).standard_normal((2, 3, 37, nx))
+    for name in KINDS:
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
+
+
+@pytest.mark.parametrize("nx,dt", [(57, "f64"), (61, "f32"), (58, "f32")])
+def test_unaligned_rows_device_path_pitched(P, nx, dt):
+    """Rows whose byte length is not a 16 B multiple run the checkpointed
+    kernels on an internal pitched copy (device applies) or pitched slots
+    (host applies); both must agree with the oracle and with each other."""
+    import torch
+    g, rx, ry = random_case(600 + nx, nx=nx, ny=45, nlev=4, sea=0.7)
+    gpu, cpu = build_pair(P, g, rx, ry)
+    f = np.random.default_rng(15).standard_normal((2, 4, 45, nx))
+    if dt == "f32":
+        f = f.astype(np.float32)
+    tol = TOL64 if dt == "f64" else TOL32
+    for name in ("GYGX", "VT", "B"):
+        host = gpu.apply(getattr(P, name), f)
+        dev = gpu.apply(getattr(P, name), torch.from_numpy(f).cuda())
+        torch.cuda.synchronize()
+        assert np.array_equal(host, dev.cpu().numpy()), name
+        want = cpu.apply(getattr(O, name), f.astype(np.float64))
+        assert relmax(host, want) <= tol, (name, relmax(host, want))
