@@ -34,7 +34,12 @@ template <typename T>
 constexpr int ck_x() {
   return 128 / int(sizeof(T));
 }
-constexpr int kCkY = 16;
+// y: 16 rows (16 warps x 32-register value arrays). 8-warp shapes with
+// 32-row blocks (half the checkpoint traffic) measured slower for fp32 too.
+template <typename T>
+constexpr int ck_y() {
+  return 16;
+}
 
 // resume a pass-A state from its raw form (raw())
 __device__ __forceinline__ void restore(FwdA2& s, double r1, double r2, double r3) {
@@ -626,7 +631,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     k_yck1(StreamArgs a, double* __restrict__ ck, const __grid_constant__ CUtensorMap tm_field,
            const __grid_constant__ CUtensorMap tm_coef, const __grid_constant__ CUtensorMap tm_idc) {
   using L = YC1<T, NW, U>;
-  constexpr int X = kCkY, SPB = X / U;
+  constexpr int X = ck_y<T>(), SPB = X / U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::bytes);
@@ -723,7 +728,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
 
 template <typename T, int NPL>
 struct YC2 {
-  static constexpr int X = kCkY;
+  static constexpr int X = ck_y<T>();
   static constexpr size_t field = size_t(NPL) * X * 32 * sizeof(T);
   static constexpr size_t coef = size_t(X) * 4 * 32 * sizeof(double);
   static constexpr size_t idc = size_t(X) * 32 * sizeof(double);
@@ -912,16 +917,22 @@ __global__ void __launch_bounds__(32 * NW, 1)
 }
 
 constexpr int kYc1NW = 16, kYc1U = 8, kYc1S = 4;
-constexpr int kYc2NW = 16, kYc2PPW = 1, kYc2S = 2;
+// C2 shapes per element type (registers: 16 warps cap them at 128)
+template <typename T>
+struct C2Shape {
+  static constexpr bool f64 = sizeof(T) == 8;
+  static constexpr int yNW = 16, yPPW = 1, yS = 2;
+  static constexpr int xR = 4, xNWR = 4, xS = 3;
+};
 constexpr int kXc1NW = 4, kXc1S = 4;
-constexpr int kXc2R = 4, kXc2NWR = 4, kXc2S = 3;
+
 
 // ------------------------------------------------------------- launchers
 template <typename T>
 int64_t ckpt_doubles(const StreamArgs& a) {
   const int64_t planes = a.nvar * a.nlev;
   if (a.dir == 0) return a.ny * ((a.nx + ck_x<T>() - 1) / ck_x<T>()) * 3 * planes;
-  return planes * ((a.ny + kCkY - 1) / kCkY) * 3 * a.nx;
+  return planes * ((a.ny + ck_y<T>() - 1) / ck_y<T>()) * 3 * a.nx;
 }
 
 template <typename T, bool TR, bool IDC, bool VAR>
@@ -959,7 +970,7 @@ void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
 
 template <typename T, bool TR, bool IDC, bool PRE, bool POST>
 void launch_xck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
-  constexpr int R = kXc2R, NWR = kXc2NWR, S = kXc2S;
+  constexpr int R = C2Shape<T>::xR, NWR = C2Shape<T>::xNWR, S = C2Shape<T>::xS;
   using L = XC2<T, R, NWR>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
@@ -1035,7 +1046,7 @@ void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
 
 template <typename T, bool TR, bool IDC, bool PRE, bool POST>
 void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
-  constexpr int NW = kYc2NW, PPW = kYc2PPW, S = kYc2S, NPL = NW * PPW;
+  constexpr int NW = C2Shape<T>::yNW, PPW = C2Shape<T>::yPPW, S = C2Shape<T>::yS, NPL = NW * PPW;
   using L = YC2<T, NPL>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
@@ -1069,7 +1080,7 @@ int launch_ck_dir(const T* in, T* out, const StreamArgs& a, double* ck, cudaStre
   const bool pre = TR && a.pre_scale != nullptr;
   const bool post = a.post_scale != nullptr;
   const int64_t n = a.dir == 0 ? a.nx : a.ny;
-  const int64_t X = a.dir == 0 ? ck_x<T>() : kCkY;
+  const int64_t X = a.dir == 0 ? ck_x<T>() : ck_y<T>();
   int launches = 0;
   // C1 (skipped when the line is a single block)
   if (n > X) {
