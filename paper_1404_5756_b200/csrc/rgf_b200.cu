@@ -24,6 +24,7 @@
 #include "sweep_stream.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_ckpt.cuh"
+#include "rf1_stream.cuh"
 #include "closures.cuh"
 
 namespace {
@@ -100,6 +101,7 @@ struct DirData {
   DevBuf<rgfb::Coef3> c3;
   DevBuf<double> c3s;  // SoA copy of c3 (y direction, checkpointed sweeps)
   DevBuf<double> idcp;  // inv_dc with even row pitch when nx is odd (TMA)
+  DevBuf<double> zone[2];  // 1st-RF ghost-zone responses per segment [fwd, adjoint]
   DevBuf<double2> c1;
   DevBuf<double> idc;
   DevBuf<int64_t> seg_off;  // nlev*lines + 1
@@ -132,6 +134,9 @@ struct rgf_op {
   // streaming 3rd-RF path: bit-packed masks, closure classes and tables
   bool stream_ok = false;
   bool ckpt_ok = true;  // checkpointed 3-pass sweeps (RGF_B200_TWOPASS=1: two-pass kernels)
+  bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
+  DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
+  DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
   DevBuf<double> ckpt;  // per-block causal checkpoints (apply scratch)
   DevBuf<uint64_t> bits[2];
   DevBuf<uint64_t> bitsT[2];  // chain-minor copies (checkpointed sweeps)
@@ -236,6 +241,31 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     return;
   }
   if (pitch != op->nx) throw std::runtime_error("sweep: pitched field on a dense-only path");
+  if (op->rf1_ok) {
+    rgfb::Rf1Args a{};
+    a.dir = dir;
+    a.transpose = transpose;
+    a.k = op->k;
+    a.nx = op->nx;
+    a.ny = op->ny;
+    a.nlev = nlev;
+    a.nvar = nvar;
+    a.lev0 = lev0;
+    a.c1 = d.c1.p;
+    a.bits = op->bits[dir].p;
+    a.seg_off = d.seg_off.p;
+    a.nsegs = d.nsegs;
+    a.zone = d.zone[transpose ? 1 : 0].p;
+    op->rf1_hist.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs * 2 * op->k)));
+    a.hist = op->rf1_hist.p;
+    op->rf1_ent.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs)));
+    a.ent = op->rf1_ent.p;
+    a.pre_scale = pre;
+    a.post_scale = post;
+    op->launches += static_cast<unsigned long long>(rgfb::launch_rf1_sweep<T>(in, out, a, st));
+    CUDA_OK(cudaGetLastError());
+    return;
+  }
 
   const int64_t n = dir == 0 ? op->nx : op->ny;
   const int64_t slab = n + 2 * op->gmax + 4;
@@ -672,6 +702,40 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
       }
     }
+    if (op->order == 1 && g->nx > 1 && g->ny > 1) {
+      const char* ex = std::getenv("RGF_B200_EXACT");
+      if (!(ex && ex[0] == '1')) {
+        // streaming 1st-RF: level-major mask bits + per-segment ghost-zone
+        // responses (forward and adjoint dynamics)
+        for (int dir = 0; dir < 2; ++dir) {
+          const int64_t n = dir == 0 ? g->nx : g->ny;
+          const int64_t nl = dir == 0 ? g->ny : g->nx;
+          op->words[dir] = (n + 63) / 64;
+          const int64_t tot = g->nlev * nl * op->words[dir];
+          op->bits[dir].alloc(tot);
+          rgfb::k_pack_bits<<<grid_for(tot, 256), 256>>>(mask.p, dir, g->nx, g->ny, g->nlev,
+                                                         op->words[dir], op->bits[dir].p);
+          CUDA_OK(cudaGetLastError());
+        }
+        const int threads = 128, blocks = 148 * 4;
+        const int64_t slab = std::max<int64_t>(1, op->gmax);
+        DevBuf<double> scr;
+        scr.alloc(static_cast<size_t>(threads) * blocks * 2 * slab);
+        for (int dir = 0; dir < 2; ++dir) {
+          DirData& d = dir == 0 ? op->dx_ : op->dy_;
+          for (int tr = 0; tr < 2; ++tr) {
+            d.zone[tr].alloc(static_cast<size_t>(std::max<int64_t>(1, d.nsegs) * 2 * op->k));
+            if (d.nsegs > 0)
+              rgfb::k_rf1_zones<<<blocks, threads>>>(d.segs.p, d.seg_line.p, d.nsegs, dir, g->nx,
+                                                     g->ny, d.c1.p, op->ghost_d.p, op->k, tr == 1,
+                                                     d.zone[tr].p, scr.p, slab);
+            CUDA_OK(cudaGetLastError());
+          }
+        }
+        CUDA_OK(cudaDeviceSynchronize());
+        op->rf1_ok = true;
+      }
+    }
     if (opt->variance) {
       op->variance.upload(opt->variance, static_cast<size_t>(nh * g->nlev));
       op->has_variance = true;
@@ -748,7 +812,8 @@ int rgf_op_device_bytes(const rgf_op* op, uint64_t* out) {
                  op->bitsT[1].bytes() + op->clos.bytes() + op->cls_d.bytes() + op->entry.bytes() +
                  op->out_d.bytes() + op->tmp1.bytes() + op->tmp2.bytes() + op->scratch.bytes();
     for (const DirData* d : {&op->dx_, &op->dy_})
-      b += d->c3.bytes() + d->c3s.bytes() + d->idcp.bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
+      b += d->c3.bytes() + d->c3s.bytes() + d->idcp.bytes() + d->zone[0].bytes() +
+           d->zone[1].bytes() + d->c1.bytes() + d->idc.bytes() + d->seg_off.bytes() + d->segs.bytes() +
            d->seg_line.bytes() + d->close_order.bytes();
     *out = b;
   });

@@ -422,3 +422,30 @@ def test_unaligned_rows_device_path_pitched(P, nx, dt):
         assert np.array_equal(host, dev.cpu().numpy()), name
         want = cpu.apply(getattr(O, name), f.astype(np.float64))
         assert relmax(host, want) <= tol, (name, relmax(host, want))
+
+
+@pytest.mark.parametrize("k", [1, 2, 5])
+def test_rf1_streaming_path(P, monkeypatch, k):
+    """The 1st-RF runs as 2K streaming passes per sweep (ghost zones folded
+    into per-segment convolutions), against the oracle and against the
+    segment-serial exact kernel (RGF_B200_EXACT=1, reference arithmetic)."""
+    g, rx, ry = random_case(800 + k, nx=70, ny=44, nlev=3, sea=0.65)
+    var = np.random.default_rng(17).uniform(0.5, 2.0, (3, 44, 70))
+    gpu, cpu = build_pair(P, g, rx, ry, order=1, k=k, variance=var)
+    monkeypatch.setenv("RGF_B200_EXACT", "1")
+    exact, _ = build_pair(P, g, rx, ry, order=1, k=k, variance=var)
+    monkeypatch.delenv("RGF_B200_EXACT")
+    import torch
+    f = np.random.default_rng(18).standard_normal((2, 3, 44, 70))
+    ft = torch.from_numpy(f).cuda()
+    for name in KINDS:
+        l0 = gpu.launch_count()
+        gpu.apply(getattr(P, name), ft)  # device path: one launch set per sweep
+        torch.cuda.synchronize()
+        sweeps = {"GX": 1, "GY": 1, "GXT": 1, "GYT": 1, "V": 2, "VT": 2, "B": 4, "GYGX": 2}[name]
+        # 2K passes + (2K-1) entry-state kernels per sweep
+        assert gpu.launch_count() - l0 == (4 * k - 1) * sweeps, (name, gpu.launch_count() - l0)
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f)
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
+        assert relmax(got, exact.apply(getattr(P, name), f)) <= TOL64, name
