@@ -41,6 +41,33 @@ constexpr int ck_y() {
   return 16;
 }
 
+// Mask words of an ascending pass, one word of lookahead: on entering word w
+// the current word is the one loaded 64 points ago (no load on the critical
+// path, no branch around a load). Word i of the line is W[i * stride].
+struct WordStream {
+  uint64_t cur = 0, nxt = 0;
+  int64_t wi = -1;
+  __device__ __forceinline__ void start(const uint64_t* W, int64_t stride, int64_t words) {
+    cur = ldw(W, 0);
+    nxt = words > 1 ? ldw(W, stride) : 0ull;
+    wi = 0;
+  }
+  // call with k0 ascending in steps that divide 64
+  __device__ __forceinline__ void advance(const uint64_t* W, int64_t stride, int64_t words,
+                                          int64_t k0) {
+    if ((k0 >> 6) != wi) {
+      wi = k0 >> 6;
+      cur = nxt;
+      const int64_t w2 = wi + 1 < words ? wi + 1 : wi;  // clamped, value unused past the end
+      nxt = ldw(W, w2 * stride);
+    }
+  }
+  template <int U>
+  __device__ __forceinline__ uint32_t stage(int64_t k0) const {
+    return static_cast<uint32_t>((cur >> (k0 & 63)) & ((1ull << U) - 1ull));
+  }
+};
+
 // resume a pass-A state from its raw form (raw())
 __device__ __forceinline__ void restore(FwdA2& s, double r1, double r2, double r3) {
   s.p1 = r1;
@@ -330,7 +357,8 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const uint64_t* W = a.bitsT + iy * a.words * a.nlev_all + lev;
   const int64_t ws = a.nlev_all;
   const double* PRE = VAR ? a.pre_scale + lev * n * ny + iy * n : nullptr;
-  StageBits sbw;
+  WordStream sbw;
+  sbw.start(W, ws, a.words);
   typename std::conditional<TR, AdjA2, FwdA2>::type st;
   uint32_t carry = 0;
   constexpr int EPC = 16 / int(sizeof(T));
@@ -339,7 +367,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
     const int64_t k0 = i * U;
-    sbw.seek(W, k0, a.words, false, ws);
+    sbw.advance(W, ws, a.words, k0);
     const uint32_t sb = sbw.stage<U>(k0);
     const uint32_t starts = sb & ~((sb << 1) | carry);
     mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
@@ -689,14 +717,15 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const int64_t ix = ix0 + (act ? lane : 0);
   const uint64_t* W = a.bitsT + lev * a.words * nx + ix;  // lanes: consecutive words
   const double* PREp = VAR ? a.pre_scale + lev * nh + ix : nullptr;
-  StageBits sbw;
+  WordStream sbw;
+  sbw.start(W, nx, a.words);
   typename std::conditional<TR, AdjA2, FwdA2>::type st;
   uint32_t carry = 0;
 
   for (int64_t i = 0; i < nst; ++i) {
     const int s = static_cast<int>(i % S);
     const int64_t lo = i * U;
-    sbw.seek(W, lo, a.words, false, nx);
+    sbw.advance(W, nx, a.words, lo);
     const uint32_t sb = sbw.stage<U>(lo);
     const uint32_t starts = sb & ~((sb << 1) | carry);
     mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
