@@ -28,6 +28,7 @@
 // work at the configs' masks).
 #pragma once
 #include "sweep_stream.cuh"
+#include "sweep_tma.cuh"
 
 namespace rgfb {
 
@@ -35,8 +36,10 @@ struct Rf1Args {
   int dir, transpose;
   int k;                      // iterations
   int64_t nx, ny, nlev, nvar, lev0;
+  int64_t nlev_all;           // levels of the operator (bitsT stride)
   const double2* c1;          // (alpha, beta) per point of this direction
   const uint64_t* bits;       // bit-packed masks (level-major)
+  const uint64_t* bitsT;      // chain-minor copy: x [iy][word][lev] (TMA kernels)
   const int64_t* seg_off;     // per (lev, line) segment prefix offsets
   int64_t nsegs;
   const double* zone;         // [seg][2K]: hL[0..K) (hL[0] = 0), cR[0..K)
@@ -418,13 +421,358 @@ __global__ void __launch_bounds__(128) k_rf1_x(const T* __restrict__ in, T* __re
   cp_async_wait<0>();
 }
 
-// K iterations of one directional sweep (2K launches): out = G_dir in.
+// ------------------------------------------------------------ TMA passes
+// Rows 16 B aligned: TMA-fed producer/consumer passes (the structure of the
+// 3rd-RF two-pass kernels, sweep_tma.cuh), one producer warp streaming
+// field and (alpha, beta) stages into an S-deep ring.
+
+// mask bit of the point after this stage in pass order
+template <int U, bool ASC>
+__device__ __forceinline__ uint32_t next_after_stage(const StageBits& b, int64_t lo) {
+  if (ASC) return b.after<U>(lo);
+  return (lo & 63) == 0 ? static_cast<uint32_t>(b.nxt >> 63)
+                        : static_cast<uint32_t>((b.cur >> ((lo - 1) & 63)) & 1ull);
+}
+
+template <typename T, int NW, int U>
+struct R1Y {
+  static constexpr size_t field = size_t(NW) * U * 32 * sizeof(T);
+  static constexpr size_t coef = size_t(U) * 64 * sizeof(double);
+  static constexpr size_t bytes = field + coef;
+};
+
+// y: 32 columns x NW planes per CTA, stages of U rows; lanes = columns,
+// warps = planes; results stored straight to global (coalesced rows)
+template <typename T, bool TR, bool ASC, bool FIRST, bool LAST, int NW, int U, int S>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    k_rf1_ytma(T* __restrict__ out, Rf1Args a, int it, const __grid_constant__ CUtensorMap tm_field,
+               const __grid_constant__ CUtensorMap tm_coef) {
+  using L = R1Y<T, NW, U>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::bytes);
+  uint64_t* empty = full + S;
+  const int64_t nx = a.nx, ny = a.ny, nh = nx * ny;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t PB = (planes + NW - 1) / NW;
+  const int64_t tile = blockIdx.x / PB;
+  const int64_t p0 = (blockIdx.x - tile * PB) * NW;
+  const int64_t ix0 = tile * 32;
+  const int ncol = static_cast<int>(nx - ix0 < 32 ? nx - ix0 : 32);
+  const int nwp = static_cast<int>(planes - p0 < NW ? planes - p0 : NW);
+  const int64_t nst = (ny + U - 1) / U;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = a.k;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], nwp);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto lo_of = [&](int64_t i) -> int64_t { return (ASC ? i : nst - 1 - i) * U; };
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+      tma_prefetch_desc(&tm_field);
+      tma_prefetch_desc(&tm_coef);
+      for (int64_t i = 0; i < nst; ++i) {
+        const int s = static_cast<int>(i % S);
+        if (i >= S) mbar_wait(&empty[s], static_cast<uint32_t>((i / S - 1) & 1));
+        const int lo = static_cast<int>(lo_of(i));
+        unsigned char* base = smem + s * L::bytes;
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(L::bytes));
+        tma_load_3d(base, &tm_field, static_cast<int>(ix0), lo, static_cast<int>(p0), &full[s],
+                    pol_stream);
+        tma_load_2d(base + L::field, &tm_coef, static_cast<int>(2 * ix0), lo, &full[s], pol_keep);
+      }
+    }
+    return;
+  }
+  if (warp >= nwp) return;
+  const int64_t p = p0 + warp;
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
+  const bool act = lane < ncol;
+  const int64_t ix = ix0 + (act ? lane : 0);
+  T* dst = out + p * nh + ix;
+  const uint64_t* W = a.bits + (lev * nx + ix) * ((ny + 63) / 64);
+  const int64_t words = (ny + 63) / 64;
+  const double* SC = nullptr;
+  if (FIRST && TR && a.pre_scale) SC = a.pre_scale + lev * nh + ix;
+  if (LAST && a.post_scale) SC = a.post_scale + lev * nh + ix;
+  double* H = a.hist + var * a.nsegs * 2 * K;
+  const double* E = a.ent + var * a.nsegs;
+  const int64_t slo = a.seg_off[lev * nx + ix], shi = a.seg_off[lev * nx + ix + 1];
+  int64_t sidx = ASC ? slo - 1 : shi;
+  auto ent_of = [&](int64_t sn) { return (sn >= slo && sn < shi) ? E[sn] : 0.0; };
+  double en = ent_of(ASC ? sidx + 1 : sidx - 1);
+  StageBits sbw;
+  Rf1Asc st;
+  uint32_t prevb = 0;  // sea bit of the previous point in pass order
+  for (int64_t i = 0; i < nst; ++i) {
+    const int s = static_cast<int>(i % S);
+    const int64_t lo = lo_of(i);
+    sbw.seek(W, lo, words, !ASC);
+    const uint32_t sb = sbw.stage<U>(lo);
+    const uint32_t nb = next_after_stage<U, ASC>(sbw, lo);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
+    const unsigned char* base = smem + s * L::bytes;
+    const T* fld = reinterpret_cast<const T*>(base) + warp * U * 32 + lane;
+    const double2* cf = reinterpret_cast<const double2*>(base + L::field) + lane;
+    const int rvalid = static_cast<int>(ny - lo < U ? ny - lo : U);
+#pragma unroll
+    for (int uu = 0; uu < U; ++uu) {
+      const int r = ASC ? uu : U - 1 - uu;
+      const int64_t k = lo + r;
+      const uint32_t sea = (sb >> r) & 1u;
+      const uint32_t nsea = ASC ? (r + 1 < U ? (sb >> (r + 1)) & 1u : nb)
+                                : (r > 0 ? (sb >> (r - 1)) & 1u : nb);
+      const double2 c = cf[r * 32];
+      double w = static_cast<double>(fld[r * 32]);
+      if (FIRST && TR && SC && r < rvalid) w *= __ldg(SC + k * nx);
+      if (sea && !prevb) {  // segment entry in pass order
+        if (ASC) ++sidx; else --sidx;
+        st.st = en;
+        st.ap = c.x;
+        en = ent_of(ASC ? sidx + 1 : sidx - 1);
+      }
+      double o = st.template step<TR>(c.x, c.y, w);
+      if (sea && !nsea && act) {
+        double* h = H + sidx * 2 * K;
+        if (ASC) h[K + it - 1] = st.st; else h[it - 1] = st.st;
+      }
+      if (LAST && SC && r < rvalid) o *= __ldg(SC + k * nx);
+      if (act && r < rvalid) __stcs(dst + k * nx, static_cast<T>(sea ? o : 0.0));
+      prevb = sea;
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+// x: one row x 32*NW planes per CTA; U-point stages of [U x 128 planes],
+// 128 B swizzled; results written back in place and returned by TMA stores
+template <typename T, bool TR, bool ASC, bool FIRST, bool LAST, int NW, int S>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    k_rf1_xtma(Rf1Args a, int it, const __grid_constant__ CUtensorMap tm_in,
+               const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ CUtensorMap tm_coef) {
+  constexpr int U = 128 / int(sizeof(T));
+  constexpr size_t FIELD = size_t(NW) * 32 * 128;
+  constexpr size_t COEF = size_t(U) * 16;
+  constexpr size_t BYTES = (FIELD + COEF + 1023) / 1024 * 1024;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * BYTES);
+  uint64_t* empty = full + S;
+  const int64_t n = a.nx, ny = a.ny, nh = n * ny;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
+  const int64_t iy = blockIdx.x / PB;
+  const int64_t p0 = (blockIdx.x - iy * PB) * 32 * NW;
+  const int npl = static_cast<int>(planes - p0 < 32 * NW ? planes - p0 : 32 * NW);
+  const int64_t nst = (n + U - 1) / U;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = a.k;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+  auto k0_of = [&](int64_t i) -> int64_t { return (ASC ? i : nst - 1 - i) * U; };
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+      tma_prefetch_desc(&tm_in);
+      tma_prefetch_desc(&tm_coef);
+      for (int64_t i = 0; i < nst; ++i) {
+        const int s = static_cast<int>(i % S);
+        if (i >= S) mbar_wait(&empty[s], static_cast<uint32_t>((i / S - 1) & 1));
+        const int k0 = static_cast<int>(k0_of(i));
+        unsigned char* base = smem + s * BYTES;
+        mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(FIELD + COEF));
+        tma_load_3d(base, &tm_in, k0, static_cast<int>(iy), static_cast<int>(p0), &full[s],
+                    pol_stream);
+        tma_load_2d(base + FIELD, &tm_coef, 2 * k0, static_cast<int>(iy), &full[s], pol_keep);
+      }
+    }
+    return;
+  }
+  const int pr = warp * 32 + lane;
+  const bool act = pr < npl;
+  const int64_t p = p0 + (act ? pr : 0);
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
+  const int64_t words = (n + 63) / 64;
+  const uint64_t* W = a.bitsT + iy * words * a.nlev_all + lev;  // lanes: consecutive words
+  const int64_t ws = a.nlev_all;
+  const double* SC = nullptr;
+  if (FIRST && TR && a.pre_scale) SC = a.pre_scale + lev * nh + iy * n;
+  if (LAST && a.post_scale) SC = a.post_scale + lev * nh + iy * n;
+  double* H = a.hist + var * a.nsegs * 2 * K;
+  const double* E = a.ent + var * a.nsegs;
+  const int64_t slo = a.seg_off[lev * ny + iy], shi = a.seg_off[lev * ny + iy + 1];
+  int64_t sidx = ASC ? slo - 1 : shi;
+  auto ent_of = [&](int64_t sn) { return (sn >= slo && sn < shi) ? E[sn] : 0.0; };
+  double en = ent_of(ASC ? sidx + 1 : sidx - 1);
+  StageBits sbw;
+  Rf1Asc st;
+  uint32_t prevb = 0;
+  constexpr int ESZ = static_cast<int>(sizeof(T));
+  constexpr int EPC = 16 / ESZ;
+  const int sw = pr & 7;
+  for (int64_t i = 0; i < nst; ++i) {
+    const int s = static_cast<int>(i % S);
+    const int64_t k0 = k0_of(i);
+    sbw.seek(W, k0, words, !ASC, ws);
+    const uint32_t sb = sbw.stage<U>(k0);
+    const uint32_t nb = next_after_stage<U, ASC>(sbw, k0);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
+    unsigned char* base = smem + s * BYTES;
+    const double2* cf = reinterpret_cast<const double2*>(base + FIELD);
+    unsigned char* rowp = base + pr * 128;
+#pragma unroll
+    for (int qq = 0; qq < U / EPC; ++qq) {
+      const int q = ASC ? qq : U / EPC - 1 - qq;
+      void* cp = rowp + ((q ^ sw) << 4);
+      double v[EPC];
+      if constexpr (sizeof(T) == 8) {
+        const double2 t = *reinterpret_cast<const double2*>(cp);
+        v[0] = t.x;
+        v[1] = t.y;
+      } else {
+        const float4 t = *reinterpret_cast<const float4*>(cp);
+        v[0] = t.x;
+        v[1] = t.y;
+        v[2] = t.z;
+        v[3] = t.w;
+      }
+#pragma unroll
+      for (int ee = 0; ee < EPC; ++ee) {
+        const int e = ASC ? ee : EPC - 1 - ee;
+        const int u = q * EPC + e;
+        const int64_t k = k0 + u;
+        const uint32_t sea = (sb >> u) & 1u;
+        const uint32_t nsea = ASC ? (u + 1 < U ? (sb >> (u + 1)) & 1u : nb)
+                                  : (u > 0 ? (sb >> (u - 1)) & 1u : nb);
+        const double2 c = cf[u];
+        double w = v[e];
+        if (FIRST && TR && SC && k < n) w *= __ldg(SC + k);
+        if (sea && !prevb) {
+          if (ASC) ++sidx; else --sidx;
+          st.st = en;
+          st.ap = c.x;
+          en = ent_of(ASC ? sidx + 1 : sidx - 1);
+        }
+        double o = st.template step<TR>(c.x, c.y, w);
+        if (sea && !nsea && act) {
+          double* h = H + sidx * 2 * K;
+          if (ASC) h[K + it - 1] = st.st; else h[it - 1] = st.st;
+        }
+        if (LAST && SC && k < n) o *= __ldg(SC + k);
+        v[e] = sea ? o : 0.0;
+        prevb = sea;
+      }
+      if constexpr (sizeof(T) == 8) {
+        *reinterpret_cast<double2*>(cp) = make_double2(v[0], v[1]);
+      } else {
+        *reinterpret_cast<float4*>(cp) =
+            make_float4(static_cast<float>(v[0]), static_cast<float>(v[1]),
+                        static_cast<float>(v[2]), static_cast<float>(v[3]));
+      }
+    }
+    fence_proxy_async_smem();
+    asm volatile("bar.sync 1, %0;\n" ::"r"(32 * NW) : "memory");
+    if (threadIdx.x == 0) {
+      tma_store_3d(&tm_out, static_cast<int>(k0), static_cast<int>(iy), static_cast<int>(p0), base,
+                   l2_evict_first());
+      bulk_commit();
+      asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory");
+      if (i > 0) mbar_arrive(&empty[(i - 1) % S]);
+    }
+  }
+  if (threadIdx.x == 0) bulk_wait_all();
+}
+
+template <typename T, bool TR, bool ASC, bool F, bool LST>
+void launch_rf1_tma(const T* src, T* dst, const Rf1Args& a, int it, cudaStream_t st) {
+  const int64_t planes = a.nvar * a.nlev;
+  const uint64_t sz = sizeof(T);
+  const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
+  const uint64_t fs[2] = {uint64_t(a.nx) * sz, uint64_t(a.nx * a.ny) * sz};
+  const uint64_t cd[2] = {uint64_t(2 * a.nx), uint64_t(a.ny)};
+  const uint64_t cs[1] = {uint64_t(2 * a.nx) * 8};
+  if (a.dir == 1) {
+    constexpr int NW = 16, U = 8, S = 4;
+    using L = R1Y<T, NW, U>;
+    const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_rf1_ytma<T, TR, ASC, F, LST, NW, U, S>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      attr = true;
+    }
+    const uint32_t fb[3] = {32, U, NW};
+    const CUtensorMap tf = make_tmap(src, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const uint32_t cb[2] = {64, U};
+    const CUtensorMap tc =
+        make_tmap(a.c1, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NW - 1) / NW);
+    k_rf1_ytma<T, TR, ASC, F, LST, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(dst, a, it, tf, tc);
+  } else {
+    constexpr int NW = 4, S = 4;
+    constexpr int U = 128 / int(sizeof(T));
+    constexpr size_t BYTES = (size_t(NW) * 32 * 128 + size_t(U) * 16 + 1023) / 1024 * 1024;
+    const size_t smem = S * BYTES + 2 * S * sizeof(uint64_t) + 1024;
+    static bool attr = false;
+    if (!attr) {
+      cudaFuncSetAttribute(k_rf1_xtma<T, TR, ASC, F, LST, NW, S>,
+                           cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      attr = true;
+    }
+    const uint32_t fb[3] = {uint32_t(U), 1, uint32_t(32 * NW)};
+    const CUtensorMap tin = make_tmap(src, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+    const CUtensorMap tout = make_tmap(dst, tma_dtype<T>(), 3, fd, fs, fb,
+                                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B);
+    const uint32_t cb[2] = {uint32_t(2 * U), 1};
+    const CUtensorMap tc =
+        make_tmap(a.c1, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb, CU_TENSOR_MAP_SWIZZLE_NONE);
+    const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
+    k_rf1_xtma<T, TR, ASC, F, LST, NW, S><<<a.ny * PB, 32 * (NW + 1), smem, st>>>(a, it, tin, tout,
+                                                                               tc);
+  }
+}
+
+// K iterations of one directional sweep (2K passes + entry-state kernels)
 template <typename T>
 int launch_rf1_sweep(const T* in, T* out, const Rf1Args& a, cudaStream_t st) {
   const int threads = 128;
   const int64_t planes = a.nvar * a.nlev;
   int launches = 0;
+  const bool tma = a.bitsT != nullptr && tma_supported(in, out, a.nx);
   auto pass = [&](bool asc, bool first, bool last, const T* src, T* dst, int it) {
+    if (tma) {
+#define RGFB_RF1T(TR, ASC, F, L) launch_rf1_tma<T, TR, ASC, F, L>(src, dst, a, it, st);
+      if (a.transpose) {
+        if (asc) {
+          if (first) { RGFB_RF1T(true, true, true, false) } else { RGFB_RF1T(true, true, false, false) }
+        } else {
+          if (last) { RGFB_RF1T(true, false, false, true) } else { RGFB_RF1T(true, false, false, false) }
+        }
+      } else {
+        if (asc) {
+          if (first) { RGFB_RF1T(false, true, true, false) } else { RGFB_RF1T(false, true, false, false) }
+        } else {
+          if (last) { RGFB_RF1T(false, false, false, true) } else { RGFB_RF1T(false, false, false, false) }
+        }
+      }
+#undef RGFB_RF1T
+      ++launches;
+      return;
+    }
 #define RGFB_RF1(TR, ASC, F, L)                                                                  \
   if (a.dir == 1) {                                                                              \
     constexpr int LL = 4, UU = 4;                                                                \

@@ -253,6 +253,8 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.lev0 = lev0;
     a.c1 = d.c1.p;
     a.bits = op->bits[dir].p;
+    a.bitsT = op->bitsT[dir].p;
+    a.nlev_all = op->nlev;
     a.seg_off = d.seg_off.p;
     a.nsegs = d.nsegs;
     a.zone = d.zone[transpose ? 1 : 0].p;
@@ -715,6 +717,10 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
           op->bits[dir].alloc(tot);
           rgfb::k_pack_bits<<<grid_for(tot, 256), 256>>>(mask.p, dir, g->nx, g->ny, g->nlev,
                                                          op->words[dir], op->bits[dir].p);
+          CUDA_OK(cudaGetLastError());
+          op->bitsT[dir].alloc(tot);  // chain-minor words for the TMA x pass
+          rgfb::k_bits_transpose<<<grid_for(tot, 256), 256>>>(
+              op->bits[dir].p, dir, g->nx, g->ny, g->nlev, op->words[dir], op->bitsT[dir].p);
           CUDA_OK(cudaGetLastError());
         }
         const int threads = 128, blocks = 148 * 4;
