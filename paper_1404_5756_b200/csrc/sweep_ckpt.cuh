@@ -946,11 +946,14 @@ __global__ void __launch_bounds__(32 * NW, 1)
 }
 
 constexpr int kYc1NW = 16, kYc1U = 8, kYc1S = 4;
-// C2 shapes per element type (registers: 16 warps cap them at 128)
+// C2 shapes (measured on C5 fp64, ncu): x 4 rows x 128 planes, 16 warps,
+// 3 buffers (3.33 ms; 3 rows/4 buffers 3.47, 2 rows/5 buffers 4.26); y 12
+// planes, 12 warps, 3 buffers (3.52 ms; 16 warps/2 buffers 3.81, 10/3
+// 3.74, 8/4 3.83, 13/3 4.22)
 template <typename T>
 struct C2Shape {
   static constexpr bool f64 = sizeof(T) == 8;
-  static constexpr int yNW = 16, yPPW = 1, yS = 2;
+  static constexpr int yNW = 12, yPPW = 1, yS = 3;
   static constexpr int xR = 4, xNWR = 4, xS = 3;
 };
 constexpr int kXc1NW = 4, kXc1S = 4;
@@ -997,9 +1000,9 @@ void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
   k_xck1<T, TR, IDC, VAR, NW, S><<<a.ny * PB, 32 * (NW + 1), smem, st>>>(a, ck, tin, tc, ti);
 }
 
-template <typename T, bool TR, bool IDC, bool PRE, bool POST>
-void launch_xck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
-  constexpr int R = C2Shape<T>::xR, NWR = C2Shape<T>::xNWR, S = C2Shape<T>::xS;
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int R, int NWR, int S>
+void launch_xck2_shape(const T* in, T* out, const StreamArgs& a, const double* ck,
+                       cudaStream_t st) {
   using L = XC2<T, R, NWR>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
@@ -1034,6 +1037,12 @@ void launch_xck2(const T* in, T* out, const StreamArgs& a, const double* ck, cud
   const int64_t blocks = ((a.ny + R - 1) / R) * PB;
   k_xck2<T, TR, IDC, PRE, POST, R, NWR, S><<<blocks, 32 * R * NWR, smem, st>>>(a, ck, tin, tout,
                                                                                tc, ti);
+}
+
+template <typename T, bool TR, bool IDC, bool PRE, bool POST>
+void launch_xck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
+  launch_xck2_shape<T, TR, IDC, PRE, POST, C2Shape<T>::xR, C2Shape<T>::xNWR, C2Shape<T>::xS>(
+      in, out, a, ck, st);
 }
 
 // paired coefficient map for the y kernels: [ny][2][nx][2] as dims
@@ -1073,9 +1082,10 @@ void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
   k_yck1<T, TR, IDC, VAR, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(a, ck, tf, tc, ti);
 }
 
-template <typename T, bool TR, bool IDC, bool PRE, bool POST>
-void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
-  constexpr int NW = C2Shape<T>::yNW, PPW = C2Shape<T>::yPPW, S = C2Shape<T>::yS, NPL = NW * PPW;
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S>
+void launch_yck2_shape(const T* in, T* out, const StreamArgs& a, const double* ck,
+                       cudaStream_t st) {
+  constexpr int NPL = NW * PPW;
   using L = YC2<T, NPL>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
@@ -1100,6 +1110,12 @@ void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cud
   const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NPL - 1) / NPL);
   k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S><<<blocks, 32 * NW, smem, st>>>(out, a, ck, tf, tc,
                                                                           ti);
+}
+
+template <typename T, bool TR, bool IDC, bool PRE, bool POST>
+void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
+  launch_yck2_shape<T, TR, IDC, PRE, POST, C2Shape<T>::yNW, C2Shape<T>::yPPW, C2Shape<T>::yS>(
+      in, out, a, ck, st);
 }
 
 // runtime flags -> template flags; returns kernel launches
