@@ -967,9 +967,8 @@ int64_t ckpt_doubles(const StreamArgs& a) {
   return planes * ((a.ny + ck_y<T>() - 1) / ck_y<T>()) * 3 * a.nx;
 }
 
-template <typename T, bool TR, bool IDC, bool VAR>
-void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) {
-  constexpr int NW = kXc1NW, S = kXc1S;
+template <typename T, bool TR, bool IDC, bool VAR, int NW, int S>
+void launch_xck1_shape(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) {
   using L = XT<T, NW, false>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
@@ -998,6 +997,13 @@ void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
                              : tc;
   const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
   k_xck1<T, TR, IDC, VAR, NW, S><<<a.ny * PB, 32 * (NW + 1), smem, st>>>(a, ck, tin, tc, ti);
+}
+
+template <typename T, bool TR, bool IDC, bool VAR>
+void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) {
+  // 4 stages, 3 CTAs/SM (1.75 ms on C5 fp64; 6 stages 1.90, 8 or 12 stages
+  // at 1 CTA/SM ~3 ms)
+  launch_xck1_shape<T, TR, IDC, VAR, kXc1NW, kXc1S>(in, a, ck, st);
 }
 
 template <typename T, bool TR, bool IDC, bool PRE, bool POST, int R, int NWR, int S>
