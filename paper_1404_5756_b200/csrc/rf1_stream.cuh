@@ -42,8 +42,9 @@ struct Rf1Args {
   const uint64_t* bitsT;      // chain-minor copy: x [iy][word][lev] (TMA kernels)
   const int64_t* seg_off;     // per (lev, line) segment prefix offsets
   int64_t nsegs;
-  const double* zone;         // [seg][2K]: hL[0..K) (hL[0] = 0), cR[0..K)
-  double* hist;               // [var][seg][2K]: x_1..x_K, y_1..y_K
+  const double* zone;         // [2K][seg]: hL[0..K) (hL[0] = 0), cR[0..K)
+  double* hist;               // [2K][var][seg]: x_1..x_K, y_1..y_K (iteration-major:
+                              // an entry-state launch reads only the slices it needs)
   double* ent;                // [var][seg]: entry state of the current pass
   const double* pre_scale;    // first pass only
   const double* post_scale;   // last pass only
@@ -71,12 +72,12 @@ __global__ void k_rf1_zones(const int2* __restrict__ segs, const int32_t* __rest
     const int gl = i > 0 ? G : 0, gr = j < n - 1 ? G : 0;
     auto pt = [&](int64_t k) { return dir == 0 ? line * nx + k : k * nx + line; };
     const double2 cl = c1[pt(i)], cr = c1[pt(j)];
-    double* z = zone + s * 2 * K;
+    double* z = zone + s;  // z[d * nsegs]
     // ---- left zone (alpha, beta of the segment's first point)
     {
       const double a = cl.x, b = cl.y;
       for (int q = 0; q < gl; ++q) g[q] = 0.0;
-      z[0] = 0.0;
+      z[0] = 0.0;  // hL[0] unused
       for (int k = 1; k <= K; ++k) {
         const double x = k == 1 ? 1.0 : 0.0;  // the impulse enters after iteration 1
         double e = 0.0;
@@ -110,7 +111,7 @@ __global__ void k_rf1_zones(const int2* __restrict__ segs, const int32_t* __rest
             prev = c;
           }
         }
-        if (k >= 2) z[k - 1] = e;  // hL[k-1]: response at iteration k to x_1
+        if (k >= 2) z[(k - 1) * nsegs] = e;  // hL[k-1]: response at iteration k to x_1
       }
     }
     // ---- right zone (alpha, beta of the segment's last point)
@@ -152,7 +153,7 @@ __global__ void k_rf1_zones(const int2* __restrict__ segs, const int32_t* __rest
           }
           e = gr > 0 ? prev : 0.0;
         }
-        z[K + k - 1] = e;  // cR[k-1]
+        z[(K + k - 1) * nsegs] = e;  // cR[k-1]
       }
     }
   }
@@ -177,16 +178,23 @@ struct Rf1Asc {
   }
 };
 
-template <bool TR>
-__device__ __forceinline__ double rf1_entry_left(const double* z, const double* hx, int it) {
+// z = zone + seg (stride zs = nsegs), h = hist + var*nsegs + seg (stride hs =
+// nvar*nsegs)
+__device__ __forceinline__ double rf1_entry_left(const double* z, int64_t zs, const double* h,
+                                                 int64_t hs, int it) {
   double e = 0.0;
-  for (int j = 1; j < it; ++j) e = fma(z[it - j], hx[j - 1], e);
+  for (int j = 1; j < it; ++j) e = fma(z[(it - j) * zs], h[(j - 1) * hs], e);
   return e;
 }
-__device__ __forceinline__ double rf1_entry_right(const double* z, const double* hy, int it, int K) {
+__device__ __forceinline__ double rf1_entry_right(const double* z, int64_t zs, const double* h,
+                                                  int64_t hs, int it, int K) {
   double e = 0.0;
-  for (int j = 1; j <= it; ++j) e = fma(z[K + it - j], hy[j - 1], e);
+  for (int j = 1; j <= it; ++j) e = fma(z[(K + it - j) * zs], h[(K + j - 1) * hs], e);
   return e;
+}
+// slot of x_it (descending exit) / y_it (ascending exit) in the history
+__device__ __forceinline__ int64_t rf1_hist_slot(bool asc, int it, int K, int64_t hs) {
+  return (asc ? K + it - 1 : it - 1) * hs;
 }
 
 // Entry states of every segment for the coming pass, from the histories
@@ -200,9 +208,10 @@ __global__ void k_rf1_entries(Rf1Args a, int it, int64_t nvar) {
   for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
        t += (int64_t)gridDim.x * blockDim.x) {
     const int64_t s = t % a.nsegs;
-    const double* z = a.zone + s * 2 * K;
-    const double* h = a.hist + t * 2 * K;
-    a.ent[t] = ASC ? rf1_entry_left<false>(z, h, it) : rf1_entry_right(z, h + K, it, K);
+    const double* z = a.zone + s;
+    const double* h = a.hist + t;
+    a.ent[t] = ASC ? rf1_entry_left(z, a.nsegs, h, total, it)
+                   : rf1_entry_right(z, a.nsegs, h, total, it, K);
   }
 }
 
@@ -241,7 +250,7 @@ __global__ void __launch_bounds__(128) k_rf1_y(const T* __restrict__ in, T* __re
     SC[l] = nullptr;
     if (FIRST && TR && a.pre_scale) SC[l] = a.pre_scale + lev * nh + ix;
     if (LAST && a.post_scale) SC[l] = a.post_scale + lev * nh + ix;
-    H[l] = a.hist + var * a.nsegs * 2 * K;
+    H[l] = a.hist + var * a.nsegs;
     sidx[l] = ASC ? a.seg_off[lev * nx + ix] - 1 : a.seg_off[lev * nx + ix + 1];
     slo[l] = a.seg_off[lev * nx + ix];
     shi[l] = a.seg_off[lev * nx + ix + 1];
@@ -308,9 +317,8 @@ __global__ void __launch_bounds__(128) k_rf1_y(const T* __restrict__ in, T* __re
         }
         double o = st[l].template step<TR>(c[u].x, c[u].y, w);
         if (sea && !nsea && on[l]) {  // segment exit in pass order: record the handed-over state
-          double* h = H[l] + sidx[l] * 2 * K;
           // ascending: y_it at the segment end; descending: x_it at its start
-          if (ASC) h[K + it - 1] = st[l].st; else h[it - 1] = st[l].st;
+          H[l][sidx[l] + rf1_hist_slot(ASC, it, K, a.nvar * a.nsegs)] = st[l].st;
         }
         if (LAST && a.post_scale) o *= sc[l][u];
         if (on[l]) dst[l][k * nx] = static_cast<T>(sea ? o : 0.0);
@@ -347,7 +355,7 @@ __global__ void __launch_bounds__(128) k_rf1_x(const T* __restrict__ in, T* __re
   if (LAST && a.post_scale) SC = a.post_scale + lev * nh + hb;
   const int64_t words = (n + 63) / 64;
   const uint64_t* W = a.bits + (lev * ny + iy) * words;
-  double* H = a.hist + var * a.nsegs * 2 * K;
+  double* H = a.hist + var * a.nsegs;
   const double* E = a.ent + var * a.nsegs;
   int64_t sidx = ASC ? a.seg_off[lev * ny + iy] - 1 : a.seg_off[lev * ny + iy + 1];
   const int64_t slo = a.seg_off[lev * ny + iy], shi = a.seg_off[lev * ny + iy + 1];
@@ -401,8 +409,7 @@ __global__ void __launch_bounds__(128) k_rf1_x(const T* __restrict__ in, T* __re
       }
       double o = st.template step<TR>(c.x, c.y, w);
       if (sea && !nsea && on) {
-        double* h = H + sidx * 2 * K;
-        if (ASC) h[K + it - 1] = st.st; else h[it - 1] = st.st;
+        H[sidx + rf1_hist_slot(ASC, it, K, a.nvar * a.nsegs)] = st.st;
       }
       if (LAST && SC) o *= __ldg(SC + k);
       row[u] = static_cast<T>(sea ? o : 0.0);
@@ -501,7 +508,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const double* SC = nullptr;
   if (FIRST && TR && a.pre_scale) SC = a.pre_scale + lev * nh + ix;
   if (LAST && a.post_scale) SC = a.post_scale + lev * nh + ix;
-  double* H = a.hist + var * a.nsegs * 2 * K;
+  double* H = a.hist + var * a.nsegs;
   const double* E = a.ent + var * a.nsegs;
   const int64_t slo = a.seg_off[lev * nx + ix], shi = a.seg_off[lev * nx + ix + 1];
   int64_t sidx = ASC ? slo - 1 : shi;
@@ -539,8 +546,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       }
       double o = st.template step<TR>(c.x, c.y, w);
       if (sea && !nsea && act) {
-        double* h = H + sidx * 2 * K;
-        if (ASC) h[K + it - 1] = st.st; else h[it - 1] = st.st;
+        H[sidx + rf1_hist_slot(ASC, it, K, a.nvar * a.nsegs)] = st.st;
       }
       if (LAST && SC && r < rvalid) o *= __ldg(SC + k * nx);
       if (act && r < rvalid) __stcs(dst + k * nx, static_cast<T>(sea ? o : 0.0));
@@ -611,7 +617,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   const double* SC = nullptr;
   if (FIRST && TR && a.pre_scale) SC = a.pre_scale + lev * nh + iy * n;
   if (LAST && a.post_scale) SC = a.post_scale + lev * nh + iy * n;
-  double* H = a.hist + var * a.nsegs * 2 * K;
+  double* H = a.hist + var * a.nsegs;
   const double* E = a.ent + var * a.nsegs;
   const int64_t slo = a.seg_off[lev * ny + iy], shi = a.seg_off[lev * ny + iy + 1];
   int64_t sidx = ASC ? slo - 1 : shi;
@@ -668,8 +674,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         }
         double o = st.template step<TR>(c.x, c.y, w);
         if (sea && !nsea && act) {
-          double* h = H + sidx * 2 * K;
-          if (ASC) h[K + it - 1] = st.st; else h[it - 1] = st.st;
+          H[sidx + rf1_hist_slot(ASC, it, K, a.nvar * a.nsegs)] = st.st;
         }
         if (LAST && SC && k < n) o *= __ldg(SC + k);
         v[e] = sea ? o : 0.0;
