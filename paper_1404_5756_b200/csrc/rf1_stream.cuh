@@ -42,6 +42,7 @@ struct Rf1Args {
   const uint64_t* bitsT;      // chain-minor copy: x [iy][word][lev] (TMA kernels)
   const int64_t* seg_off;     // per (lev, line) segment prefix offsets
   int64_t nsegs;
+  int64_t seg_begin, seg_end;  // segments of this launch's levels
   const double* zone;         // [2K][seg]: hL[0..K) (hL[0] = 0), cR[0..K)
   double* hist;               // [2K][var][seg]: x_1..x_K, y_1..y_K (iteration-major:
                               // an entry-state launch reads only the slices it needs)
@@ -201,13 +202,17 @@ __device__ __forceinline__ int64_t rf1_hist_slot(bool asc, int it, int K, int64_
 // (one thread per (var, segment), coalesced), so a pass only loads one value
 // per segment entry -- prefetched a segment ahead -- instead of a dependent
 // K-term sum on scattered memory.
+// Only the segments of this launch's levels [s0, s1) (segments are stored
+// level-major, so a level chunk's segments are contiguous).
 template <bool ASC>
-__global__ void k_rf1_entries(Rf1Args a, int it, int64_t nvar) {
+__global__ void k_rf1_entries(Rf1Args a, int it, int64_t s0, int64_t s1) {
   const int K = a.k;
-  const int64_t total = nvar * a.nsegs;
-  for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
-       t += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t s = t % a.nsegs;
+  const int64_t total = a.nvar * a.nsegs;  // history stride
+  const int64_t span = s1 - s0;
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < a.nvar * span;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = q / span, s = s0 + (q - v * span);
+    const int64_t t = v * a.nsegs + s;
     const double* z = a.zone + s;
     const double* h = a.hist + t;
     a.ent[t] = ASC ? rf1_entry_left(z, a.nsegs, h, total, it)
@@ -811,18 +816,24 @@ int launch_rf1_sweep(const T* in, T* out, const Rf1Args& a, cudaStream_t st) {
 #undef RGFB_RF1
     ++launches;
   };
-  const int64_t ne = a.nvar * a.nsegs;
+  // this launch's segments: levels [lev0, lev0 + nlev) of every line
+  const int64_t nlines = a.dir == 0 ? a.ny : a.nx;
+  const int64_t s0 = a.seg_begin, s1 = a.seg_end;
+  (void)nlines;
+  const int64_t ne = a.nvar * (s1 - s0);
   const int eblocks = static_cast<int>(std::min<int64_t>((ne + 255) / 256, 148 * 16));
   for (int it = 1; it <= a.k; ++it) {
     if (it > 1 && ne > 0) {  // iteration 1 enters every segment from zero
-      k_rf1_entries<true><<<eblocks, 256, 0, st>>>(a, it, a.nvar);
+      k_rf1_entries<true><<<eblocks, 256, 0, st>>>(a, it, s0, s1);
       ++launches;
     } else if (ne > 0) {
-      cudaMemsetAsync(a.ent, 0, static_cast<size_t>(ne) * sizeof(double), st);
+      for (int64_t v = 0; v < a.nvar; ++v)
+        cudaMemsetAsync(a.ent + v * a.nsegs + s0, 0, static_cast<size_t>(s1 - s0) * sizeof(double),
+                        st);
     }
     pass(true, it == 1, false, it == 1 ? in : out, out, it);
     if (ne > 0) {
-      k_rf1_entries<false><<<eblocks, 256, 0, st>>>(a, it, a.nvar);
+      k_rf1_entries<false><<<eblocks, 256, 0, st>>>(a, it, s0, s1);
       ++launches;
     }
     pass(false, false, it == a.k, out, out, it);

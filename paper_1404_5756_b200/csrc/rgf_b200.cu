@@ -105,6 +105,7 @@ struct DirData {
   DevBuf<double2> c1;
   DevBuf<double> idc;
   DevBuf<int64_t> seg_off;  // nlev*lines + 1
+  std::vector<int64_t> seg_off_h;  // host copy (1st-RF level-chunk segment ranges)
   DevBuf<int2> segs;
   DevBuf<int32_t> seg_line;  // per segment: lev*lines + line
   DevBuf<int64_t> close_order;  // segments sorted by (line, end, level)
@@ -257,6 +258,11 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.nlev_all = op->nlev;
     a.seg_off = d.seg_off.p;
     a.nsegs = d.nsegs;
+    {  // this launch's level range as a segment range (host copy of seg_off)
+      const int64_t nl = dir == 0 ? op->ny : op->nx;
+      a.seg_begin = d.seg_off_h[static_cast<size_t>(lev0 * nl)];
+      a.seg_end = d.seg_off_h[static_cast<size_t>((lev0 + nlev) * nl)];
+    }
     a.zone = d.zone[transpose ? 1 : 0].p;
     op->rf1_hist.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs * 2 * op->k)));
     a.hist = op->rf1_hist.p;
@@ -369,6 +375,11 @@ void apply_host_pipelined(rgf_op* op, int kind, const T* hin, T* hout, int64_t n
   if (const char* e = std::getenv("RGF_B200_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));
   int64_t cl = std::max<int64_t>(1, (chunk_mb << 20) / per_level);
   cl = std::min(cl, std::max<int64_t>(1, (nlev + 3) / 4));
+  // The x kernels give each lane a plane and walk a whole row per CTA, so a
+  // sweep over a few planes costs nearly as much as over 128. The 3rd-RF's
+  // four kernels per chunk hide under the PCIe copies; the 1st-RF's 2K passes
+  // per sweep do not, so its chunks hold at least 32 levels.
+  if (op->order == 1) cl = std::max<int64_t>(cl, 32);
   cl = std::min(cl, nlev);
   constexpr int kSlots = 3;
   op->pipe_init();
@@ -456,8 +467,10 @@ void build_segments(rgf_op* op, const uint8_t* mask_d, int dir, DirData& d) {
   DevBuf<char> tmp;
   tmp.alloc(tmp_bytes);
   CUDA_OK(cub::DeviceScan::InclusiveSum(tmp.p, tmp_bytes, counts.p, d.seg_off.p + 1, lines));
-  int64_t total = 0;
-  CUDA_OK(cudaMemcpy(&total, d.seg_off.p + lines, sizeof(int64_t), cudaMemcpyDeviceToHost));
+  d.seg_off_h.resize(static_cast<size_t>(lines + 1));
+  CUDA_OK(cudaMemcpy(d.seg_off_h.data(), d.seg_off.p, (lines + 1) * sizeof(int64_t),
+                     cudaMemcpyDeviceToHost));
+  const int64_t total = d.seg_off_h[static_cast<size_t>(lines)];
   d.nsegs = total;
   d.segs.alloc(std::max<int64_t>(total, 1));
   d.seg_line.alloc(std::max<int64_t>(total, 1));
