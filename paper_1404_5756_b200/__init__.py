@@ -32,7 +32,7 @@ __all__ = [
 ]
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "librgf_b200.so")
+LIB_PATH = os.environ.get("RGF_B200_LIB") or os.path.join(_HERE, "librgf_b200.so")  # dev override
 
 if not os.path.exists(LIB_PATH):  # fail loudly: the product has no fallback
     raise ImportError(

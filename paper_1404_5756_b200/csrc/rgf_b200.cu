@@ -24,6 +24,7 @@
 #include "sweep_stream.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_ckpt.cuh"
+#include "sweep_ring.cuh"
 #include "rf1_stream.cuh"
 #include "closures.cuh"
 
@@ -135,6 +136,7 @@ struct rgf_op {
   // streaming 3rd-RF path: bit-packed masks, closure classes and tables
   bool stream_ok = false;
   bool ckpt_ok = true;  // checkpointed 3-pass sweeps (RGF_B200_TWOPASS=1: two-pass kernels)
+  bool ring_ok = false;  // single-pass ring sweeps (experimental: RGF_B200_SWEEP=ring)
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
@@ -229,6 +231,11 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.entry = op->entry.p;
     a.pre_scale = pre;
     a.post_scale = post;
+    if (op->ckpt_ok && op->ring_ok && rgfb::tma_supported(in, out, pitch)) {
+      op->launches += static_cast<unsigned long long>(rgfb::launch_ring_sweep<T>(in, out, a, st));
+      CUDA_OK(cudaGetLastError());
+      return;
+    }
     if (op->ckpt_ok && rgfb::tma_supported(in, out, pitch)) {
       op->ckpt.alloc(static_cast<size_t>(std::max<int64_t>(1, rgfb::ckpt_doubles<T>(a))));
       op->launches +=
@@ -506,6 +513,18 @@ extern "C" {
 
 const char* rgf_last_error(void) { return g_last_error.c_str(); }
 
+#ifdef RGF_RING_PROF
+// development build only: per-section cycle totals of the ring sweeps
+int rgf_debug_ring_prof(unsigned long long* out, int reset) {
+  if (cudaMemcpyFromSymbol(out, rgfb::g_ring_prof, 8 * sizeof(unsigned long long)) != cudaSuccess) return 1;
+  if (reset) {
+    const unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    if (cudaMemcpyToSymbol(rgfb::g_ring_prof, z, sizeof(z)) != cudaSuccess) return 1;
+  }
+  return 0;
+}
+#endif
+
 void rgf_options_default(rgf_options* o) {
   o->order = RGF_ORDER_THIRD;
   o->k_iterations = 1;
@@ -695,6 +714,8 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         op->stream_ok = true;
         const char* tp = std::getenv("RGF_B200_TWOPASS");
         op->ckpt_ok = !(tp && tp[0] == '1');
+        const char* sv = std::getenv("RGF_B200_SWEEP");
+        op->ring_ok = sv && std::strcmp(sv, "ring") == 0;
         if (op->ckpt_ok) {
           for (int dir = 0; dir < 2; ++dir) {
             const int64_t tot = g->nlev * (dir == 0 ? g->ny : g->nx) * op->words[dir];

@@ -449,3 +449,27 @@ def test_rf1_streaming_path(P, monkeypatch, k):
         want = cpu.apply(getattr(O, name), f)
         assert relmax(got, want) <= TOL64, (name, relmax(got, want))
         assert relmax(got, exact.apply(getattr(P, name), f)) <= TOL64, name
+
+
+@pytest.mark.parametrize("nx,ny,sea,dt", [(96, 37, 0.8, "f64"), (400, 300, 1.0, "f64"),
+                                          (57, 43, 0.6, "f64"), (128, 70, 0.8, "f32")])
+def test_ring_sweeps_experimental(P, monkeypatch, nx, ny, sea, dt):
+    """RGF_B200_SWEEP=ring selects the single-pass ring kernels (sweep_ring.cuh,
+    experimental). Per-level masks (warp lanes meet different segment ends),
+    all-sea lines longer than the ring (spills through the output buffer), and
+    unaligned rows (pitched copies), for every kind."""
+    g, rx, ry = random_case(611 + nx, nx=nx, ny=ny, nlev=5, sea=sea)
+    var = np.random.default_rng(15).uniform(0.5, 2.0, (5, ny, nx))
+    monkeypatch.setenv("RGF_B200_SWEEP", "ring")
+    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
+    monkeypatch.delenv("RGF_B200_SWEEP")
+    f = np.random.default_rng(16).standard_normal((2, 5, ny, nx))
+    tol = TOL64
+    if dt == "f32":
+        f = f.astype(np.float32)
+        tol = TOL32
+    for name in KINDS:
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f.astype(np.float64))
+        assert relmax(got, want) <= tol, (name, relmax(got, want))
+        assert np.all(got[:, ~g["mask"]] == 0.0), name
