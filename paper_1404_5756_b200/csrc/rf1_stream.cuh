@@ -41,6 +41,8 @@ struct Rf1Args {
   const uint64_t* bits;       // bit-packed masks (level-major)
   const uint64_t* bitsT;      // chain-minor copy: x [iy][word][lev] (TMA kernels)
   const int64_t* seg_off;     // per (lev, line) segment prefix offsets
+  const int2* segs;           // (start, len) per segment (line-resident kernel)
+  const int32_t* lpt_ord;     // segments of each line, longest first (k_rf1_sort)
   int64_t nsegs;
   int64_t seg_begin, seg_end;  // segments of this launch's levels
   const double* zone;         // [2K][seg]: hL[0..K) (hL[0] = 0), cR[0..K)

@@ -26,6 +26,7 @@
 #include "sweep_ckpt.cuh"
 #include "sweep_ring.cuh"
 #include "rf1_stream.cuh"
+#include "rf1_seg.cuh"
 #include "closures.cuh"
 
 namespace {
@@ -109,6 +110,8 @@ struct DirData {
   std::vector<int64_t> seg_off_h;  // host copy (1st-RF level-chunk segment ranges)
   DevBuf<int2> segs;
   DevBuf<int32_t> seg_line;  // per segment: lev*lines + line
+  DevBuf<int32_t> lpt_ord;   // 1st-RF line-resident kernel: each line's segments, longest first
+  int lpt_B = 0;             // lpt_ord built
   DevBuf<int64_t> close_order;  // segments sorted by (line, end, level)
   int64_t nsegs = 0;
   std::vector<char> uniform;        // per level
@@ -264,6 +267,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.bitsT = op->bitsT[dir].p;
     a.nlev_all = op->nlev;
     a.seg_off = d.seg_off.p;
+    a.segs = d.segs.p;
     a.nsegs = d.nsegs;
     {  // this launch's level range as a segment range (host copy of seg_off)
       const int64_t nl = dir == 0 ? op->ny : op->nx;
@@ -277,6 +281,28 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.ent = op->rf1_ent.p;
     a.pre_scale = pre;
     a.post_scale = post;
+    // line-resident kernel (all K iterations in one pass, experimental:
+    // RGF_B200_RF1=line) when the line group fits in shared memory; the
+    // 2K-pass streaming kernels are the default (faster)
+    const char* rv = std::getenv("RGF_B200_RF1");
+    const bool seg = rv && std::strcmp(rv, "line") == 0;
+    if (seg) {  // per-line segment order (longest first), built on first use
+      DirData& dm = dir == 0 ? op->dx_ : op->dy_;
+      const int64_t nl = op->nlev * (dir == 0 ? op->ny : op->nx);
+      if (!dm.lpt_B && dm.nsegs > 0) {
+        dm.lpt_ord.alloc(static_cast<size_t>(dm.nsegs));
+        rgfb::k_rf1_sort<<<grid_for(nl, 128, 148 * 16), 128, 0, st>>>(dm.seg_off.p, dm.segs.p, nl,
+                                                                    dm.lpt_ord.p);
+        CUDA_OK(cudaGetLastError());
+        dm.lpt_B = 1;
+      }
+      if (dm.lpt_B) a.lpt_ord = dm.lpt_ord.p;
+    }
+    if (seg && a.lpt_ord != nullptr && rgfb::launch_rf1_seg<T>(in, out, a, st)) {
+      op->launches += 1;
+      CUDA_OK(cudaGetLastError());
+      return;
+    }
     op->launches += static_cast<unsigned long long>(rgfb::launch_rf1_sweep<T>(in, out, a, st));
     CUDA_OK(cudaGetLastError());
     return;

@@ -473,3 +473,36 @@ def test_ring_sweeps_experimental(P, monkeypatch, nx, ny, sea, dt):
         want = cpu.apply(getattr(O, name), f.astype(np.float64))
         assert relmax(got, want) <= tol, (name, relmax(got, want))
         assert np.all(got[:, ~g["mask"]] == 0.0), name
+
+
+@pytest.mark.parametrize("k,nx,ny,sea,dt", [(1, 70, 44, 0.65, "f64"), (3, 64, 40, 0.8, "f64"),
+                                             (5, 96, 57, 0.6, "f64"), (5, 64, 300, 1.0, "f64"),
+                                             (5, 64, 37, 0.7, "f32"), (8, 32, 20, 0.7, "f64")])
+def test_rf1_line_resident_matches_streaming(P, monkeypatch, k, nx, ny, sea, dt):
+    """The line-resident 1st-RF (rf1_seg.cuh, experimental RGF_B200_RF1=line:
+    a line group in shared memory, lanes = segments, all K iterations, one
+    launch per sweep) is bit-identical to the 2K-pass streaming kernels (the
+    default) and matches the oracle, for every kind, with variance, per-level
+    masks, 300-row columns (several 256-row TMA boxes) and fp32 storage."""
+    import torch
+    g, rx, ry = random_case(830 + k + nx, nx=nx, ny=ny, nlev=3, sea=sea)
+    var = np.random.default_rng(19).uniform(0.5, 2.0, (3, ny, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, order=1, k=k, variance=var)
+    f = np.random.default_rng(20).standard_normal((2, 3, ny, nx))
+    if dt == "f32":
+        f = f.astype(np.float32)
+    ft = torch.from_numpy(f).cuda()
+    for name in KINDS:
+        monkeypatch.setenv("RGF_B200_RF1", "line")  # read per apply
+        l0 = gpu.launch_count()
+        got = gpu.apply(getattr(P, name), ft)
+        torch.cuda.synchronize()
+        sweeps = {"GX": 1, "GY": 1, "GXT": 1, "GYT": 1, "V": 2, "VT": 2, "B": 4, "GYGX": 2}[name]
+        assert gpu.launch_count() - l0 == sweeps, (name, gpu.launch_count() - l0)
+        got = got.cpu().numpy()
+        monkeypatch.delenv("RGF_B200_RF1")
+        ref = gpu.apply(getattr(P, name), ft).cpu().numpy()
+        assert np.array_equal(got, ref), (name, relmax(got, ref))
+        want = cpu.apply(getattr(O, name), f.astype(np.float64))
+        assert relmax(got, want) <= (TOL64 if dt == "f64" else TOL32), (name, relmax(got, want))
+        assert np.all(got[:, ~g["mask"]] == 0.0), name
