@@ -164,17 +164,28 @@ struct AdjA2 {
 
 // One-word-lookahead mask window, advanced once per stage. Stages never
 // straddle a 64-bit word (U divides 64 and stages start at multiples of U).
+// Two words of lookahead: `nxt` (the word after `cur` in pass order) arrived
+// a word ago and `nn` (the one after it) is in flight, so neither the stage
+// bits nor the after-stage bit ever wait on a load issued at this word
+// change (a select on a fresh load stalled the 1st-RF passes ~25%).
 struct StageBits {
   int64_t wi = -1;
-  uint64_t cur = 0, nxt = 0;
+  uint64_t cur = 0, nxt = 0, nn = 0;
   // word i of the line at W[i * stride]
   __device__ __forceinline__ void seek(const uint64_t* W, int64_t k, int64_t words, bool desc,
                                        int64_t stride = 1) {
     const int64_t w = k >> 6;
     if (w == wi) return;
-    cur = (wi >= 0 && w == (desc ? wi - 1 : wi + 1)) ? nxt : ldw(W, w * stride);
-    const int64_t wn = desc ? w - 1 : w + 1;
-    nxt = (wn >= 0 && wn < words) ? ldw(W, wn * stride) : 0ull;
+    const int64_t step = desc ? -1 : 1;
+    const int64_t w1 = w + step, w2 = w + 2 * step;
+    if (wi >= 0 && w == wi + step) {
+      cur = nxt;
+      nxt = (w1 >= 0 && w1 < words) ? nn : 0ull;  // nn was loaded a word ago
+    } else {  // first word of the pass
+      cur = ldw(W, w * stride);
+      nxt = (w1 >= 0 && w1 < words) ? ldw(W, w1 * stride) : 0ull;
+    }
+    nn = ldw(W, (w2 < 0 ? 0 : (w2 >= words ? words - 1 : w2)) * stride);  // masked at shift
     wi = w;
   }
   template <int U>
