@@ -150,6 +150,44 @@ int rgf_rf3_apply_1d(const double* in, const double* sigma, int64_t m, int64_t n
 int rgf_rf1_apply_1d(const double* in, const double* sigma, int64_t m, int64_t nlines,
                      int k, int transpose, double* out);
 
+
+/* ------------------------------------------------------------------------
+ * Observation operator and 3D-VAR analysis, on an
+ * operator with one level. Replaces obs.hpp:15-46 (ObsSet, obs_operator,
+ * obs_operator_transpose, misfit) and solver.hpp:19-55 (SolveOptions,
+ * Analysis, cost, solve). Positions are fractional grid indices (x, y);
+ * fields are ny*nx doubles, x fastest. Errors: RGF_EINVAL with the
+ * reference's messages ("observation n: ...", "solve: tol must be
+ * positive", "solve: max_iter must be >= 0").
+ * ------------------------------------------------------------------------ */
+typedef struct rgf_obs rgf_obs;
+
+typedef struct rgf_analysis {
+  int32_t cg_iterations;
+  int32_t converged;
+  int64_t n_gradient_norms; /* initial residual + one per iteration */
+  double final_relative_residual;
+  double j_background;
+  double j_obs;
+} rgf_analysis;
+
+/* obs.cpp:18-57: stencils validated here (bilinear_stencil messages) */
+int rgf_obs_create(rgf_op* op, int64_t n, const double* x, const double* y,
+                   const double* values, const double* r_var, rgf_obs** out);
+int rgf_obs_destroy(rgf_obs* obs);
+/* transpose 0: out[n] = H in (field); 1: out (field) = H^T in[n];
+ * memory RGF_HOST | RGF_DEVICE */
+int rgf_obs_apply(rgf_op* op, rgf_obs* obs, int transpose, const double* in, double* out,
+                  int memory, void* stream);
+/* solver.cpp:35-50 (host arrays): j3 = {J, J_b, J_o}; background may be NULL */
+int rgf_cost(rgf_op* op, rgf_obs* obs, const double* chi, const double* background,
+             double* j3, double* gradient);
+/* solver.cpp:52-114 (host arrays): increment (field), misfit (n, may be
+ * NULL), gradient_norms (max_iter + 1 slots); background may be NULL */
+int rgf_solve(rgf_op* op, rgf_obs* obs, double tol, int32_t max_iter,
+              const double* background, double* increment, double* misfit,
+              double* gradient_norms, rgf_analysis* out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -51,6 +51,11 @@ lib.rgfo_op_ghost_width.argtypes = [_vp, _i64]
 lib.rgfo_op_ghost_width.restype = _i64
 lib.rgfo_op_coefficient_bytes.argtypes = [_vp]
 lib.rgfo_op_coefficient_bytes.restype = ctypes.c_uint64
+lib.rgfo_obs_create.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, _vp]
+lib.rgfo_obs_destroy.argtypes = [_vp]
+lib.rgfo_obs_apply.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp]
+lib.rgfo_cost.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+lib.rgfo_solve.argtypes = [_vp, _vp, _d, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 lib.rgfo_op_uniform.argtypes = [_vp, _i64, ctypes.c_int]
 lib.rgfo_resolve_thread_count.argtypes = [ctypes.c_int]
 
@@ -172,3 +177,60 @@ class OracleOp:
         out = np.empty_like(f)
         _check(lib.rgfo_op_apply(self._h, kind, _p(f), _p(out), nvar, lev0, nlev_sub))
         return out
+
+
+# ------------------------------------------------------------- obs + CG
+class OracleObs:
+    """ObsSet on a one-level OracleOp (obs.cpp:18-93): positions (n, 2) in
+    fractional grid indices (x, y), values, r_var."""
+
+    def __init__(self, op, positions, values, r_var):
+        pos = np.asarray(positions, dtype=np.float64).reshape(-1, 2)
+        self.op = op
+        self.n = pos.shape[0]
+        self._keep = [np.ascontiguousarray(pos[:, 0]), np.ascontiguousarray(pos[:, 1]),
+                      np.ascontiguousarray(values, dtype=np.float64),
+                      np.ascontiguousarray(r_var, dtype=np.float64)]
+        h = _vp()
+        _check(lib.rgfo_obs_create(op._h, self.n, *(_p(a) for a in self._keep), ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            lib.rgfo_obs_destroy(self._h)
+            self._h = None
+
+    def h(self, field):
+        f = np.ascontiguousarray(field, dtype=np.float64)
+        out = np.empty(self.n)
+        _check(lib.rgfo_obs_apply(self.op._h, self._h, 0, _p(f), _p(out)))
+        return out
+
+    def ht(self, vec):
+        v = np.ascontiguousarray(vec, dtype=np.float64)
+        out = np.empty((self.op.ny, self.op.nx))
+        _check(lib.rgfo_obs_apply(self.op._h, self._h, 1, _p(v), _p(out)))
+        return out
+
+    def cost(self, chi, background=None):
+        c = np.ascontiguousarray(chi, dtype=np.float64)
+        bg = None if background is None else np.ascontiguousarray(background, dtype=np.float64)
+        j3 = np.empty(3)
+        g = np.empty_like(c)
+        _check(lib.rgfo_cost(self.op._h, self._h, _p(c), None if bg is None else _p(bg), _p(j3),
+                             _p(g)))
+        return {"j_total": j3[0], "j_background": j3[1], "j_obs": j3[2], "gradient": g}
+
+    def solve(self, tol=1e-6, max_iter=30, background=None):
+        bg = None if background is None else np.ascontiguousarray(background, dtype=np.float64)
+        inc = np.empty((self.op.ny, self.op.nx))
+        mis = np.empty(max(self.n, 1))
+        gn = np.empty(max_iter + 1)
+        info = np.zeros(3, dtype=np.int64)
+        out3 = np.empty(3)
+        _check(lib.rgfo_solve(self.op._h, self._h, float(tol), int(max_iter),
+                              None if bg is None else _p(bg), _p(inc), _p(mis), _p(gn),
+                              info.ctypes.data_as(ctypes.c_void_p), _p(out3)))
+        return {"increment": inc, "misfit": mis[:self.n], "cg_iterations": int(info[0]),
+                "converged": bool(info[1]), "gradient_norms": gn[:int(info[2])],
+                "final_relative_residual": out3[0], "j_background": out3[1], "j_obs": out3[2]}

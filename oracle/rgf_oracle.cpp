@@ -883,3 +883,248 @@ int rgfo_op_uniform(const rgfo_op* op, int64_t level, int dir) {
 int rgfo_resolve_thread_count(int requested) { return resolve_thread_count(requested); }
 
 }  // extern "C"
+
+// ------------------------------------------------------------------ obs + CG
+// Restatement of obs.cpp (bilinear H, scatter H^T, misfit) and solver.cpp
+// (cost, control-variable CG) for a 2-D operator (level 0, one variable).
+namespace {
+
+struct Stencil {
+  Index i0, j0;
+  double w00, w10, w01, w11;
+};
+
+}  // namespace
+
+struct rgfo_obs {
+  Index n = 0;
+  std::vector<Stencil> st;
+  std::vector<double> values, r_var;
+};
+
+namespace {
+
+// obs.cpp:18-44 bilinear_stencil
+Stencil bilinear_stencil(const rgfo_op* op, double x, double y, Index row) {
+  const auto fail = [row](const std::string& why) {
+    throw std::invalid_argument("observation " + std::to_string(row) + ": " + why);
+  };
+  if (!std::isfinite(x) || !std::isfinite(y) || x < 0 || y < 0 || x > double(op->nx - 1) ||
+      y > double(op->ny - 1))
+    fail("position (" + std::to_string(x) + "," + std::to_string(y) + ") is outside the grid");
+  Stencil st;
+  st.i0 = std::min<Index>(static_cast<Index>(std::floor(x)), op->nx - 2);
+  st.j0 = std::min<Index>(static_cast<Index>(std::floor(y)), op->ny - 2);
+  const double fx = x - double(st.i0);
+  const double fy = y - double(st.j0);
+  st.w00 = (1 - fx) * (1 - fy);
+  st.w10 = fx * (1 - fy);
+  st.w01 = (1 - fx) * fy;
+  st.w11 = fx * fy;
+  const bool any_sea = op->sea(0, st.i0, st.j0) || op->sea(0, st.i0 + 1, st.j0) ||
+                       op->sea(0, st.i0, st.j0 + 1) || op->sea(0, st.i0 + 1, st.j0 + 1);
+  if (!any_sea) fail("all four stencil corners are land");
+  return st;
+}
+
+// obs.cpp:59-71
+void obs_h(const rgfo_op* op, const rgfo_obs* o, const double* f, double* out) {
+  const Index nx = op->nx;
+  for (Index n = 0; n < o->n; ++n) {
+    const Stencil& st = o->st[n];
+    const Index c = st.j0 * nx + st.i0;
+    out[n] = st.w00 * f[c] + st.w10 * f[c + 1] + st.w01 * f[c + nx] + st.w11 * f[c + nx + 1];
+  }
+}
+
+// obs.cpp:73-87
+void obs_ht(const rgfo_op* op, const rgfo_obs* o, const double* v, double* out) {
+  const Index nx = op->nx;
+  std::fill(out, out + op->nx * op->ny, 0.0);
+  for (Index n = 0; n < o->n; ++n) {
+    const Stencil& st = o->st[n];
+    const Index c = st.j0 * nx + st.i0;
+    out[c] += st.w00 * v[n];
+    out[c + 1] += st.w10 * v[n];
+    out[c + nx] += st.w01 * v[n];
+    out[c + nx + 1] += st.w11 * v[n];
+  }
+}
+
+double odot(const std::vector<double>& a, const std::vector<double>& b) {
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+void validate_obs(const rgfo_obs* o) {  // obs.cpp:48-57 (positions checked at creation)
+  for (Index n = 0; n < o->n; ++n)
+    if (!(o->r_var[n] > 0))
+      throw std::invalid_argument("observation " + std::to_string(n) +
+                                  ": error variance must be positive");
+}
+
+struct CgCtx {
+  const rgfo_op* op;
+  const rgfo_obs* o;
+  Index nh;
+  std::vector<double> apply(int kind, const std::vector<double>& x) const {
+    std::vector<double> y(nh);
+    if (rgfo_op_apply(op, kind, x.data(), y.data(), 1, 0, 0) != 0)
+      throw std::runtime_error(rgfo_last_error());
+    return y;
+  }
+  std::vector<double> h(const std::vector<double>& f) const {
+    std::vector<double> y(o->n);
+    obs_h(op, o, f.data(), y.data());
+    return y;
+  }
+  // solver.cpp:26-31: V^T H^T (v ./ r_var)
+  std::vector<double> adjoint_rhs(const std::vector<double>& v) const {
+    std::vector<double> s(o->n), t(nh);
+    for (Index n = 0; n < o->n; ++n) s[n] = v[n] / o->r_var[n];
+    obs_ht(op, o, s.data(), t.data());
+    return apply(5, t);
+  }
+  // solver.cpp:18-22
+  std::vector<double> misfit(const double* background) const {
+    if (!background) return o->values;
+    std::vector<double> bg(background, background + nh);
+    std::vector<double> hb = h(bg), d(o->n);
+    for (Index n = 0; n < o->n; ++n) d[n] = o->values[n] - hb[n];
+    return d;
+  }
+};
+
+void require_2d(const rgfo_op* op) {
+  if (op->nlev != 1) throw std::invalid_argument("solve: the operator must have one level");
+}
+
+}  // namespace
+
+extern "C" {
+
+int rgfo_obs_create(const rgfo_op* op, int64_t n, const double* x, const double* y,
+                    const double* values, const double* r_var, rgfo_obs** out) {
+  return guarded([&] {
+    require_2d(op);
+    auto o = std::make_unique<rgfo_obs>();
+    o->n = n;
+    for (Index k = 0; k < n; ++k) o->st.push_back(bilinear_stencil(op, x[k], y[k], k));
+    o->values.assign(values, values + n);
+    o->r_var.assign(r_var, r_var + n);
+    *out = o.release();
+  });
+}
+
+void rgfo_obs_destroy(rgfo_obs* o) { delete o; }
+
+// transpose 0: out[n] = H field; 1: out field = H^T in
+int rgfo_obs_apply(const rgfo_op* op, const rgfo_obs* o, int transpose, const double* in,
+                   double* out) {
+  return guarded([&] {
+    if (transpose)
+      obs_ht(op, o, in, out);
+    else
+      obs_h(op, o, in, out);
+  });
+}
+
+// solver.cpp:35-50; j3 = {j_total, j_background, j_obs}
+int rgfo_cost(const rgfo_op* op, const rgfo_obs* o, const double* chi, const double* background,
+              double* j3, double* gradient) {
+  return guarded([&] {
+    require_2d(op);
+    validate_obs(o);
+    const CgCtx cx{op, o, op->nx * op->ny};
+    const std::vector<double> d = cx.misfit(background);
+    const std::vector<double> c(chi, chi + cx.nh);
+    const std::vector<double> hv = cx.h(cx.apply(4, c));
+    std::vector<double> res(o->n);
+    for (Index n = 0; n < o->n; ++n) res[n] = d[n] - hv[n];
+    const double jb = 0.5 * odot(c, c);
+    double jo = 0.0;
+    for (Index n = 0; n < o->n; ++n) jo += res[n] * res[n] / o->r_var[n];
+    jo *= 0.5;
+    j3[0] = jb + jo;
+    j3[1] = jb;
+    j3[2] = jo;
+    const std::vector<double> g = cx.adjoint_rhs(res);
+    for (Index p = 0; p < cx.nh; ++p) gradient[p] = c[p] - g[p];
+  });
+}
+
+// solver.cpp:52-114. gnorms: max_iter + 1 slots; info = {iterations, converged,
+// number of gradient norms}; out3 = {final_relative_residual, j_background, j_obs}
+int rgfo_solve(const rgfo_op* op, const rgfo_obs* o, double tol, int max_iter,
+               const double* background, double* increment, double* misfit, double* gnorms,
+               int64_t* info, double* out3) {
+  return guarded([&] {
+    if (!(tol > 0)) throw std::invalid_argument("solve: tol must be positive");
+    if (max_iter < 0) throw std::invalid_argument("solve: max_iter must be >= 0");
+    require_2d(op);
+    validate_obs(o);
+    const CgCtx cx{op, o, op->nx * op->ny};
+    std::fill(increment, increment + cx.nh, 0.0);
+    const std::vector<double> d = cx.misfit(background);
+    std::copy(d.begin(), d.end(), misfit);
+    info[0] = 0;
+    info[1] = 0;
+    info[2] = 0;
+    out3[0] = out3[1] = out3[2] = 0.0;
+    if (o->n == 0) {
+      info[1] = 1;
+      return;
+    }
+    const std::vector<double> b = cx.adjoint_rhs(d);
+    const double bnorm = std::sqrt(odot(b, b));
+    if (bnorm == 0) {
+      info[1] = 1;
+      return;
+    }
+    std::vector<double> chi(cx.nh, 0.0), r = b, p = r;
+    double rs = odot(r, r);
+    std::vector<double> gn{std::sqrt(rs)};
+    bool conv = false;
+    int iters = 0;
+    for (int it = 0; it < max_iter; ++it) {
+      std::vector<double> ap = cx.adjoint_rhs(cx.h(cx.apply(4, p)));  // solver.cpp:81-85
+      for (Index q = 0; q < cx.nh; ++q) ap[q] = p[q] + ap[q];
+      const double denom = odot(p, ap);
+      if (denom <= 0) break;
+      const double alpha = rs / denom;
+      for (Index q = 0; q < cx.nh; ++q) chi[q] += alpha * p[q];
+      for (Index q = 0; q < cx.nh; ++q) r[q] -= alpha * ap[q];
+      const double rs_next = odot(r, r);
+      iters = it + 1;
+      gn.push_back(std::sqrt(rs_next));
+      if (std::sqrt(rs_next) <= tol * bnorm) {
+        conv = true;
+        rs = rs_next;
+        break;
+      }
+      const double beta = rs_next / rs;
+      for (Index q = 0; q < cx.nh; ++q) p[q] = r[q] + beta * p[q];
+      rs = rs_next;
+    }
+    (void)conv;
+    const double rel = gn.back() / bnorm;
+    const std::vector<double> inc = cx.apply(4, chi);
+    std::copy(inc.begin(), inc.end(), increment);
+    const std::vector<double> hi = cx.h(inc);
+    double jo = 0.0;
+    for (Index n = 0; n < o->n; ++n) {
+      const double res = d[n] - hi[n];
+      jo += res * res / o->r_var[n];
+    }
+    info[0] = iters;
+    info[1] = rel <= tol ? 1 : 0;
+    info[2] = static_cast<int64_t>(gn.size());
+    std::copy(gn.begin(), gn.end(), gnorms);
+    out3[0] = rel;
+    out3[1] = 0.5 * odot(chi, chi);
+    out3[2] = 0.5 * jo;
+  });
+}
+
+}  // extern "C"

@@ -70,6 +70,20 @@ uint64_t rgfo_op_coefficient_bytes(const rgfo_op* op);
 int rgfo_op_uniform(const rgfo_op* op, int64_t level, int dir);
 int rgfo_resolve_thread_count(int requested);
 
+/* Observation operator and CG analysis (obs.cpp, solver.cpp) on a one-level
+ * operator: positions x, y in fractional grid indices; fields ny*nx. */
+typedef struct rgfo_obs rgfo_obs;
+int rgfo_obs_create(const rgfo_op* op, int64_t n, const double* x, const double* y,
+                    const double* values, const double* r_var, rgfo_obs** out);
+void rgfo_obs_destroy(rgfo_obs* o);
+int rgfo_obs_apply(const rgfo_op* op, const rgfo_obs* o, int transpose, const double* in,
+                   double* out);
+int rgfo_cost(const rgfo_op* op, const rgfo_obs* o, const double* chi, const double* background,
+              double* j3, double* gradient);
+int rgfo_solve(const rgfo_op* op, const rgfo_obs* o, double tol, int max_iter,
+               const double* background, double* increment, double* misfit, double* gnorms,
+               int64_t* info, double* out3);
+
 #ifdef __cplusplus
 }
 #endif

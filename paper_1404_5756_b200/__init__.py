@@ -420,3 +420,165 @@ def rf1_apply_1d(x, sigma, k):
 
 def rf1_apply_transpose_1d(x, sigma, k):
     return _apply_1d(lib.rgf_rf1_apply_1d, x, sigma, int(k), 1)
+
+
+# --------------------------------------------------------------------------
+# Observation operator and 3D-VAR analysis, mirroring
+# obs.hpp:15-46 and solver.hpp:19-55 on a one-level operator. H and H^T run on
+# the device bit-identically to the reference (deterministic gather for H^T);
+# the CG loop keeps chi, r, p, Ap on the device, one scalar per dot product
+# comes back per step.
+class _Analysis(ctypes.Structure):
+    _fields_ = [("cg_iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("n_gradient_norms", _i64), ("final_relative_residual", ctypes.c_double),
+                ("j_background", ctypes.c_double), ("j_obs", ctypes.c_double)]
+
+
+lib.rgf_obs_create.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]
+lib.rgf_obs_destroy.argtypes = [_vp]
+lib.rgf_obs_apply.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp, ctypes.c_int, _vp]
+lib.rgf_cost.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
+lib.rgf_solve.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp, _vp, _vp,
+                          ctypes.POINTER(_Analysis)]
+
+
+@dataclass
+class ObsSet:
+    """obs.hpp:15-25: positions (n, 2) fractional grid indices (x, y), values,
+    per-observation error variances."""
+    positions: np.ndarray
+    values: np.ndarray
+    r_var: np.ndarray
+
+    def size(self) -> int:
+        return int(np.asarray(self.values).size)
+
+
+@dataclass
+class SolveOptions:
+    """solver.hpp:19-22."""
+    tol: float = 1e-6
+    max_iter: int = 30
+
+
+@dataclass
+class Analysis:
+    """solver.hpp:24-33."""
+    increment: np.ndarray
+    misfit: np.ndarray
+    cg_iterations: int
+    gradient_norms: list
+    converged: bool
+    final_relative_residual: float
+    j_background: float
+    j_obs: float
+
+
+@dataclass
+class CostReport:
+    """solver.hpp:35-40."""
+    j_total: float
+    j_background: float
+    j_obs: float
+    gradient: np.ndarray
+
+
+class _DeviceObs:
+    """rgf_obs handle: stencils validated on creation (obs.cpp:18-44)."""
+
+    def __init__(self, op: "HorizontalCovarianceOp", obs: ObsSet):
+        pos = np.asarray(obs.positions, dtype=np.float64).reshape(-1, 2)
+        vals = np.ascontiguousarray(obs.values, dtype=np.float64).reshape(-1)
+        rv = np.ascontiguousarray(obs.r_var, dtype=np.float64).reshape(-1)
+        if not (pos.shape[0] == vals.size == rv.size):
+            raise InvalidArgument("ObsSet: inconsistent column lengths")
+        self.n = vals.size
+        self._keep = [np.ascontiguousarray(pos[:, 0]), np.ascontiguousarray(pos[:, 1]), vals, rv]
+        h = _vp()
+        _check(lib.rgf_obs_create(op._h, self.n, *(_ptr(a) for a in self._keep),
+                                  ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h and lib is not None:
+            lib.rgf_obs_destroy(h)
+            self._h = None
+
+
+def _field2d(op, f):
+    f = np.ascontiguousarray(f, dtype=np.float64)
+    if f.size != op.grid().nx * op.grid().ny:
+        raise InvalidArgument("field does not match the grid")
+    return f.reshape(op.grid().ny, op.grid().nx)
+
+
+def obs_operator(field, obs: ObsSet, op: "HorizontalCovarianceOp") -> np.ndarray:
+    """H: bilinear interpolation at each observation (obs.cpp:59-71)."""
+    f = _field2d(op, field)
+    d = _DeviceObs(op, obs)
+    out = np.empty(d.n)
+    if d.n:
+        _check(lib.rgf_obs_apply(op._h, d._h, 0, _ptr(f), _ptr(out), 0, None))
+    return out
+
+
+def obs_operator_transpose(vec, obs: ObsSet, op: "HorizontalCovarianceOp") -> np.ndarray:
+    """H^T: scatter with the same bilinear weights (obs.cpp:73-87)."""
+    v = np.ascontiguousarray(vec, dtype=np.float64).reshape(-1)
+    d = _DeviceObs(op, obs)
+    if v.size != d.n:
+        raise InvalidArgument("obs_operator_transpose: vector length mismatch")
+    g = op.grid()
+    out = np.empty((g.ny, g.nx))
+    _check(lib.rgf_obs_apply(op._h, d._h, 1, _ptr(v) if v.size else _ptr(out), _ptr(out), 0,
+                             None))
+    return out
+
+
+def misfit(background_at_obs, obs: ObsSet) -> np.ndarray:
+    """d = y - H(x_b) (obs.cpp:89-93)."""
+    b = np.asarray(background_at_obs, dtype=np.float64).reshape(-1)
+    y = np.asarray(obs.values, dtype=np.float64).reshape(-1)
+    if b.size != y.size:
+        raise InvalidArgument("misfit: vector length mismatch")
+    return y - b
+
+
+def cost(chi, obs: ObsSet, op: "HorizontalCovarianceOp", background=None) -> CostReport:
+    """J(chi) and its gradient (solver.cpp:35-50)."""
+    c = _field2d(op, chi)
+    bg = None if background is None else _field2d(op, background)
+    d = _DeviceObs(op, obs)
+    j3 = np.empty(3)
+    grad = np.empty_like(c)
+    _check(lib.rgf_cost(op._h, d._h, _ptr(c), None if bg is None else _ptr(bg), _ptr(j3),
+                        _ptr(grad)))
+    return CostReport(float(j3[0]), float(j3[1]), float(j3[2]), grad)
+
+
+def solve(obs: ObsSet, op: "HorizontalCovarianceOp", options: SolveOptions = SolveOptions(),
+          background=None) -> Analysis:
+    """CG on (I + V^T H^T R^-1 H V) chi = V^T H^T R^-1 d, increment V chi
+    (solver.cpp:52-114), on the device."""
+    if not (options.tol > 0):
+        raise InvalidArgument("solve: tol must be positive")
+    if options.max_iter < 0:
+        raise InvalidArgument("solve: max_iter must be >= 0")
+    bg = None if background is None else _field2d(op, background)
+    d = _DeviceObs(op, obs)
+    g = op.grid()
+    inc = np.empty((g.ny, g.nx))
+    mis = np.empty(max(d.n, 1))
+    gn = np.empty(options.max_iter + 1)
+    an = _Analysis()
+    _check(lib.rgf_solve(op._h, d._h, float(options.tol), int(options.max_iter),
+                         None if bg is None else _ptr(bg), _ptr(inc), _ptr(mis), _ptr(gn),
+                         ctypes.byref(an)))
+    return Analysis(inc, mis[:d.n].copy(), int(an.cg_iterations),
+                    list(gn[:an.n_gradient_norms]), bool(an.converged),
+                    float(an.final_relative_residual), float(an.j_background), float(an.j_obs))
+
+
+__all__ += ["ObsSet", "SolveOptions", "Analysis", "CostReport", "obs_operator",
+            "obs_operator_transpose", "misfit", "cost", "solve"]

@@ -28,6 +28,7 @@
 #include "rf1_stream.cuh"
 #include "rf1_seg.cuh"
 #include "closures.cuh"
+#include "solver_kernels.cuh"
 
 namespace {
 
@@ -124,6 +125,7 @@ struct rgf_op {
   int device = 0;
   int64_t nx = 0, ny = 0, nlev = 0;
   int order = 3, k = 1, unit_dc = 1, calibration = 0;
+  std::vector<uint8_t> mask0;  // level-0 mask on the host (observation stencils, obs.cpp:38-41)
   std::vector<int64_t> ghost;  // per level
   int64_t gmax = 0;
   DevBuf<int> ghost_d;
@@ -535,6 +537,117 @@ void build_segments(rgf_op* op, const uint8_t* mask_d, int dir, DirData& d) {
 
 }  // namespace
 
+// ---------------------------------------------------------- observations + CG
+// the observation operator (obs.cpp) and the
+// control-variable CG analysis (solver.cpp) kept on the device. Stencils are
+// validated and built on the host with the reference's formulas; the
+// per-iteration work (V, V^T sweeps, H, H^T, dots, updates) runs on the GPU.
+struct rgf_obs {
+  int device = 0;
+  int64_t n = 0, nx = 0, ny = 0;
+  std::vector<double> values_h, rvar_h;
+  DevBuf<int64_t> cell;
+  DevBuf<double4> w;
+  DevBuf<double> values, rvar;
+  // H^T gather lists: touched cells, CSR offsets, (obs*4 + corner) entries
+  int64_t ncell = 0;
+  DevBuf<int64_t> tcells, tptr;
+  DevBuf<int32_t> tent;
+};
+
+namespace {
+
+int blocks_for(int64_t n) { return grid_for(std::max<int64_t>(n, 1), 256, 148 * 8); }
+
+// obs.cpp:18-44
+void obs_stencil(const rgf_op* op, double x, double y, int64_t row, int64_t& i0, int64_t& j0,
+                 double4& w) {
+  const auto fail = [row](const std::string& why) {
+    throw InvalidArgument("observation " + std::to_string(row) + ": " + why);
+  };
+  if (!std::isfinite(x) || !std::isfinite(y) || x < 0 || y < 0 || x > double(op->nx - 1) ||
+      y > double(op->ny - 1))
+    fail("position (" + std::to_string(x) + "," + std::to_string(y) + ") is outside the grid");
+  i0 = std::min<int64_t>(static_cast<int64_t>(std::floor(x)), op->nx - 2);
+  j0 = std::min<int64_t>(static_cast<int64_t>(std::floor(y)), op->ny - 2);
+  const double fx = x - double(i0), fy = y - double(j0);
+  w = make_double4((1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy);
+  const auto sea = [&](int64_t i, int64_t j) { return op->mask0[j * op->nx + i] != 0; };
+  if (!(sea(i0, j0) || sea(i0 + 1, j0) || sea(i0, j0 + 1) || sea(i0 + 1, j0 + 1)))
+    fail("all four stencil corners are land");
+}
+
+struct Cg {
+  rgf_op* op;
+  rgf_obs* o;
+  cudaStream_t st;
+  int64_t nh;
+  DevBuf<double> partial, scal, tmp_obs, tmp_obs2, tmp_f;
+  void init() {
+    partial.alloc(rgfb::kDotBlocks);
+    scal.alloc(1);
+    tmp_obs.alloc(std::max<int64_t>(o->n, 1));
+    tmp_obs2.alloc(std::max<int64_t>(o->n, 1));
+    tmp_f.alloc(nh);
+  }
+  // a.b, or sum a^2 / r (r != nullptr)
+  double dot(const double* a, const double* b, int64_t n, const double* r = nullptr) {
+    rgfb::k_dot1<<<rgfb::kDotBlocks, rgfb::kDotThreads, 0, st>>>(a, b, r, n, partial.p);
+    rgfb::k_dot2<<<1, rgfb::kDotThreads, 0, st>>>(partial.p, rgfb::kDotBlocks, scal.p);
+    CUDA_OK(cudaGetLastError());
+    double h = 0.0;
+    CUDA_OK(cudaMemcpyAsync(&h, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+    op->launches += 2;
+    return h;
+  }
+  void h(const double* f, double* out) {
+    if (o->n == 0) return;
+    rgfb::k_obs_h<<<blocks_for(o->n), 256, 0, st>>>(f, o->n, o->nx, o->cell.p, o->w.p, out);
+    CUDA_OK(cudaGetLastError());
+    op->launches += 1;
+  }
+  void ht(const double* v, const double* rvar, double* out) {
+    CUDA_OK(cudaMemsetAsync(out, 0, static_cast<size_t>(nh) * sizeof(double), st));
+    if (o->ncell == 0) return;
+    rgfb::k_obs_ht<<<blocks_for(o->ncell), 256, 0, st>>>(
+        v, rvar, o->ncell, o->tcells.p, o->tptr.p, o->tent.p,
+        reinterpret_cast<const double*>(o->w.p), out);
+    CUDA_OK(cudaGetLastError());
+    op->launches += 1;
+  }
+  void v(const double* in, double* out) { apply_device<double>(op, RGF_V, in, out, 1, st); }
+  // solver.cpp:26-31: V^T H^T (v ./ r_var)
+  void adjoint_rhs(const double* vobs, double* out) {
+    ht(vobs, o->rvar.p, tmp_f.p);
+    apply_device<double>(op, RGF_VT, tmp_f.p, out, 1, st);
+  }
+  // solver.cpp:18-22: d = y (no background) or y - H x_b
+  void misfit(const double* bg_dev, double* d) {
+    if (o->n == 0) return;
+    if (!bg_dev) {
+      CUDA_OK(cudaMemcpyAsync(d, o->values.p, o->n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      return;
+    }
+    h(bg_dev, tmp_obs2.p);
+    rgfb::k_obs_residual<<<blocks_for(o->n), 256, 0, st>>>(o->values.p, tmp_obs2.p, o->n, d);
+    CUDA_OK(cudaGetLastError());
+    op->launches += 1;
+  }
+};
+
+void check_cg_op(const rgf_op* op) {
+  if (op->nlev != 1) throw InvalidArgument("solve: the operator must have one level");
+}
+void validate_rvar(const rgf_obs* o) {  // obs.cpp:48-57 (positions checked at creation)
+  for (int64_t k = 0; k < o->n; ++k)
+    if (!(o->rvar_h[static_cast<size_t>(k)] > 0))
+      throw InvalidArgument("observation " + std::to_string(k) +
+                            ": error variance must be positive");
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* rgf_last_error(void) { return g_last_error.c_str(); }
@@ -593,6 +706,7 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
     rxd.upload(rx, nh);
     ryd.upload(ry, nh);
     mask.upload(g->mask, static_cast<size_t>(nh * g->nlev));
+    op->mask0.assign(g->mask, g->mask + nh);
     any_sea.alloc(nh);
     flag.alloc(1);
 
@@ -1021,6 +1135,236 @@ int rgf_rf1_apply_1d(const double* in, const double* sigma, int64_t m, int64_t n
     if (m < 2) throw InvalidArgument("rf1 filter: segment length must be >= 2");
     if (nlines < 1) throw InvalidArgument("rf1 filter: nlines must be >= 1");
     apply_1d(in, sigma, m, nlines, 1, k, RGF_CAL_YVV95, transpose, out);
+  });
+}
+
+
+// ------------------------------------------------------------ observations
+int rgf_obs_create(rgf_op* op, int64_t n, const double* x, const double* y, const double* values,
+                   const double* r_var, rgf_obs** out) {
+  return guarded([&] {
+    if (!op || !out) throw InvalidArgument("obs: null argument");
+    if (n < 0) throw InvalidArgument("ObsSet: inconsistent column lengths");
+    if (n > 0 && (!x || !y || !values || !r_var)) throw InvalidArgument("obs: null argument");
+    if (n >= (int64_t(1) << 29)) throw InvalidArgument("obs: too many observations");
+    check_cg_op(op);
+    std::lock_guard<std::mutex> lock(op->mu);
+    CUDA_OK(cudaSetDevice(op->device));
+    auto o = std::make_unique<rgf_obs>();
+    o->device = op->device;
+    o->n = n;
+    o->nx = op->nx;
+    o->ny = op->ny;
+    std::vector<int64_t> cell(static_cast<size_t>(n));
+    std::vector<double4> w(static_cast<size_t>(n));
+    for (int64_t k = 0; k < n; ++k) {
+      int64_t i0, j0;
+      obs_stencil(op, x[k], y[k], k, i0, j0, w[static_cast<size_t>(k)]);
+      cell[static_cast<size_t>(k)] = j0 * op->nx + i0;
+    }
+    o->values_h.assign(values, values + n);
+    o->rvar_h.assign(r_var, r_var + n);
+    // H^T gather lists in observation order (counting sort by cell)
+    const int64_t nh = op->nx * op->ny;
+    std::vector<int64_t> cnt(static_cast<size_t>(nh) + 1, 0);
+    auto corner = [&](int64_t k, int q) {
+      const int64_t c = cell[static_cast<size_t>(k)];
+      return c + (q & 1) + (q >> 1) * op->nx;
+    };
+    for (int64_t k = 0; k < n; ++k)
+      for (int q = 0; q < 4; ++q) ++cnt[static_cast<size_t>(corner(k, q)) + 1];
+    std::vector<int64_t> tcells, tptr{0};
+    std::vector<int64_t> pos(static_cast<size_t>(nh), -1);
+    for (int64_t c = 0; c < nh; ++c)
+      if (cnt[static_cast<size_t>(c) + 1] > 0) {
+        pos[static_cast<size_t>(c)] = static_cast<int64_t>(tcells.size());
+        tcells.push_back(c);
+        tptr.push_back(tptr.back() + cnt[static_cast<size_t>(c) + 1]);
+      }
+    std::vector<int32_t> tent(static_cast<size_t>(4 * n));
+    std::vector<int64_t> fill(tcells.size(), 0);
+    for (int64_t k = 0; k < n; ++k)
+      for (int q = 0; q < 4; ++q) {
+        const int64_t t = pos[static_cast<size_t>(corner(k, q))];
+        tent[static_cast<size_t>(tptr[static_cast<size_t>(t)] + fill[static_cast<size_t>(t)]++)] =
+            static_cast<int32_t>(4 * k + q);
+      }
+    o->ncell = static_cast<int64_t>(tcells.size());
+    if (n > 0) {
+      o->cell.upload(cell.data(), cell.size());
+      o->w.upload(w.data(), w.size());
+      o->values.upload(values, static_cast<size_t>(n));
+      o->rvar.upload(r_var, static_cast<size_t>(n));
+      o->tcells.upload(tcells.data(), tcells.size());
+      o->tptr.upload(tptr.data(), tptr.size());
+      o->tent.upload(tent.data(), tent.size());
+    }
+    *out = o.release();
+  });
+}
+
+int rgf_obs_destroy(rgf_obs* o) {
+  return guarded([&] {
+    if (o) {
+      cudaSetDevice(o->device);
+      delete o;
+    }
+  });
+}
+
+// transpose 0: out (n) = H in (ny*nx field); 1: out (field) = H^T in (n)
+int rgf_obs_apply(rgf_op* op, rgf_obs* o, int transpose, const double* in, double* out,
+                  int memory, void* stream) {
+  return guarded([&] {
+    if (!op || !o || !in || !out) throw InvalidArgument("obs: null argument");
+    std::lock_guard<std::mutex> lock(op->mu);
+    CUDA_OK(cudaSetDevice(op->device));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    Cg cg{op, o, st, op->nx * op->ny, {}, {}, {}, {}, {}};
+    const int64_t nin = transpose ? o->n : cg.nh, nout = transpose ? cg.nh : o->n;
+    DevBuf<double> di, dout;
+    const double* src = in;
+    double* dst = out;
+    if (memory == RGF_HOST) {
+      di.alloc(std::max<int64_t>(nin, 1));
+      dout.alloc(std::max<int64_t>(nout, 1));
+      if (nin > 0)
+        CUDA_OK(cudaMemcpyAsync(di.p, in, nin * sizeof(double), cudaMemcpyHostToDevice, st));
+      src = di.p;
+      dst = dout.p;
+    } else if (memory != RGF_DEVICE) {
+      throw InvalidArgument("obs: unknown memory kind");
+    }
+    if (transpose)
+      cg.ht(src, nullptr, dst);
+    else
+      cg.h(src, dst);
+    if (memory == RGF_HOST && nout > 0)
+      CUDA_OK(cudaMemcpyAsync(out, dst, nout * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+// solver.cpp:35-50 (host arrays): j3 = {j_total, j_background, j_obs}
+int rgf_cost(rgf_op* op, rgf_obs* o, const double* chi, const double* background, double* j3,
+             double* gradient) {
+  return guarded([&] {
+    if (!op || !o || !chi || !j3 || !gradient) throw InvalidArgument("cost: null argument");
+    check_cg_op(op);
+    validate_rvar(o);
+    std::lock_guard<std::mutex> lock(op->mu);
+    CUDA_OK(cudaSetDevice(op->device));
+    cudaStream_t st = nullptr;
+    Cg cg{op, o, st, op->nx * op->ny, {}, {}, {}, {}, {}};
+    cg.init();
+    const int64_t nh = cg.nh, n = o->n;
+    DevBuf<double> c, bg, d, vc, res, g;
+    c.upload(chi, static_cast<size_t>(nh));
+    if (background) bg.upload(background, static_cast<size_t>(nh));
+    d.alloc(std::max<int64_t>(n, 1));
+    res.alloc(std::max<int64_t>(n, 1));
+    vc.alloc(nh);
+    g.alloc(nh);
+    cg.misfit(background ? bg.p : nullptr, d.p);
+    cg.v(c.p, vc.p);  // solver.cpp:41
+    cg.h(vc.p, cg.tmp_obs.p);
+    if (n > 0) {
+      rgfb::k_obs_residual<<<blocks_for(n), 256, 0, st>>>(d.p, cg.tmp_obs.p, n, res.p);
+      CUDA_OK(cudaGetLastError());
+    }
+    const double jb = 0.5 * cg.dot(c.p, c.p, nh);
+    const double jo = n > 0 ? 0.5 * cg.dot(res.p, nullptr, n, o->rvar.p) : 0.0;
+    cg.adjoint_rhs(res.p, g.p);
+    rgfb::k_axmy<<<blocks_for(nh), 256, 0, st>>>(g.p, c.p, g.p, 1.0, nh);  // chi - V^T H^T R^-1 r
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpy(gradient, g.p, nh * sizeof(double), cudaMemcpyDeviceToHost));
+    j3[0] = jb + jo;
+    j3[1] = jb;
+    j3[2] = jo;
+  });
+}
+
+// solver.cpp:52-114 (host arrays). gnorms: max_iter + 1 slots.
+int rgf_solve(rgf_op* op, rgf_obs* o, double tol, int32_t max_iter, const double* background,
+              double* increment, double* misfit, double* gnorms, rgf_analysis* out) {
+  return guarded([&] {
+    if (!(tol > 0)) throw InvalidArgument("solve: tol must be positive");
+    if (max_iter < 0) throw InvalidArgument("solve: max_iter must be >= 0");
+    if (!op || !o || !increment || !out || !gnorms) throw InvalidArgument("solve: null argument");
+    check_cg_op(op);
+    validate_rvar(o);
+    std::lock_guard<std::mutex> lock(op->mu);
+    CUDA_OK(cudaSetDevice(op->device));
+    cudaStream_t st = nullptr;
+    Cg cg{op, o, st, op->nx * op->ny, {}, {}, {}, {}, {}};
+    cg.init();
+    const int64_t nh = cg.nh, n = o->n;
+    *out = rgf_analysis{};
+    std::fill(increment, increment + nh, 0.0);
+    DevBuf<double> bg, d;
+    d.alloc(std::max<int64_t>(n, 1));
+    if (background) bg.upload(background, static_cast<size_t>(nh));
+    cg.misfit(background ? bg.p : nullptr, d.p);
+    if (n > 0 && misfit)
+      CUDA_OK(cudaMemcpy(misfit, d.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+    if (n == 0) {
+      out->converged = 1;
+      return;
+    }
+    DevBuf<double> b, chi, r, p, ap, t;
+    for (DevBuf<double>* v : {&b, &chi, &r, &p, &ap, &t}) v->alloc(nh);
+    const int blk = blocks_for(nh);
+    cg.adjoint_rhs(d.p, b.p);
+    const double bnorm = std::sqrt(cg.dot(b.p, b.p, nh));
+    if (bnorm == 0) {
+      out->converged = 1;
+      return;
+    }
+    CUDA_OK(cudaMemsetAsync(chi.p, 0, nh * sizeof(double), st));
+    CUDA_OK(cudaMemcpyAsync(r.p, b.p, nh * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    CUDA_OK(cudaMemcpyAsync(p.p, r.p, nh * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    double rs = cg.dot(r.p, r.p, nh);
+    std::vector<double> gn{std::sqrt(rs)};
+    int iters = 0;
+    for (int it = 0; it < max_iter; ++it) {
+      cg.v(p.p, t.p);  // apply_hessian, solver.cpp:81-85
+      cg.h(t.p, cg.tmp_obs.p);
+      cg.adjoint_rhs(cg.tmp_obs.p, ap.p);
+      rgfb::k_add<<<blk, 256, 0, st>>>(ap.p, p.p, ap.p, nh);
+      const double denom = cg.dot(p.p, ap.p, nh);
+      if (denom <= 0) break;
+      const double alpha = rs / denom;
+      rgfb::k_axpy<<<blk, 256, 0, st>>>(chi.p, chi.p, p.p, alpha, nh);
+      rgfb::k_axmy<<<blk, 256, 0, st>>>(r.p, r.p, ap.p, alpha, nh);
+      CUDA_OK(cudaGetLastError());
+      op->launches += 3;
+      const double rs_next = cg.dot(r.p, r.p, nh);
+      iters = it + 1;
+      gn.push_back(std::sqrt(rs_next));
+      if (std::sqrt(rs_next) <= tol * bnorm) {
+        rs = rs_next;
+        break;
+      }
+      rgfb::k_axpy<<<blk, 256, 0, st>>>(p.p, r.p, p.p, rs_next / rs, nh);
+      CUDA_OK(cudaGetLastError());
+      op->launches += 1;
+      rs = rs_next;
+    }
+    const double rel = gn.back() / bnorm;
+    cg.v(chi.p, t.p);  // increment = V chi
+    cg.h(t.p, cg.tmp_obs.p);
+    rgfb::k_obs_residual<<<blocks_for(n), 256, 0, st>>>(d.p, cg.tmp_obs.p, n, cg.tmp_obs2.p);
+    CUDA_OK(cudaGetLastError());
+    const double jb = 0.5 * cg.dot(chi.p, chi.p, nh);
+    const double jo = 0.5 * cg.dot(cg.tmp_obs2.p, nullptr, n, o->rvar.p);
+    CUDA_OK(cudaMemcpy(increment, t.p, nh * sizeof(double), cudaMemcpyDeviceToHost));
+    std::copy(gn.begin(), gn.end(), gnorms);
+    out->cg_iterations = iters;
+    out->converged = rel <= tol ? 1 : 0;
+    out->n_gradient_norms = static_cast<int64_t>(gn.size());
+    out->final_relative_residual = rel;
+    out->j_background = jb;
+    out->j_obs = jo;
   });
 }
 
