@@ -171,14 +171,16 @@ typedef struct rgf_analysis {
   double j_obs;
 } rgf_analysis;
 
-/* obs.cpp:18-57: stencils validated here (bilinear_stencil messages) */
-int rgf_obs_create(rgf_op* op, int64_t n, const double* x, const double* y,
-                   const double* values, const double* r_var, rgf_obs** out);
+/* obs.cpp:18-57: an ObsSet bound to a grid (level-0 mask) on a device;
+ * stencils validated here (bilinear_stencil messages) */
+int rgf_obs_create(const rgf_grid_desc* grid, int32_t device, int64_t n, const double* x,
+                   const double* y, const double* values, const double* r_var,
+                   rgf_obs** out);
 int rgf_obs_destroy(rgf_obs* obs);
-/* transpose 0: out[n] = H in (field); 1: out (field) = H^T in[n];
- * memory RGF_HOST | RGF_DEVICE */
-int rgf_obs_apply(rgf_op* op, rgf_obs* obs, int transpose, const double* in, double* out,
-                  int memory, void* stream);
+/* transpose 0: out[n] = H in (field, obs.cpp:59-71); 1: out (field) = H^T
+ * in[n] (obs.cpp:73-87); memory RGF_HOST | RGF_DEVICE */
+int rgf_obs_apply(rgf_obs* obs, int transpose, const double* in, double* out, int memory,
+                  void* stream);
 /* solver.cpp:35-50 (host arrays): j3 = {J, J_b, J_o}; background may be NULL */
 int rgf_cost(rgf_op* op, rgf_obs* obs, const double* chi, const double* background,
              double* j3, double* gradient);

@@ -213,6 +213,7 @@ class HorizontalCovarianceOp {
 
   const Grid2D& grid() const { return *grid_; }
   const CovarianceOptions& options() const { return options_; }
+  rgf_op* handle() const { return op_; }  // the C-ABI operator (solver.hpp)
   Index effective_ghost_width() const {
     int64_t g = 0;
     detail::check(rgf_op_ghost_width(op_, 0, &g));

@@ -434,9 +434,10 @@ class _Analysis(ctypes.Structure):
                 ("j_background", ctypes.c_double), ("j_obs", ctypes.c_double)]
 
 
-lib.rgf_obs_create.argtypes = [_vp, _i64, _vp, _vp, _vp, _vp, ctypes.POINTER(_vp)]
+lib.rgf_obs_create.argtypes = [_vp, ctypes.c_int32, _i64, _vp, _vp, _vp, _vp,
+                               ctypes.POINTER(_vp)]
 lib.rgf_obs_destroy.argtypes = [_vp]
-lib.rgf_obs_apply.argtypes = [_vp, _vp, ctypes.c_int, _vp, _vp, ctypes.c_int, _vp]
+lib.rgf_obs_apply.argtypes = [_vp, ctypes.c_int, _vp, _vp, ctypes.c_int, _vp]
 lib.rgf_cost.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
 lib.rgf_solve.argtypes = [_vp, _vp, ctypes.c_double, ctypes.c_int32, _vp, _vp, _vp, _vp,
                           ctypes.POINTER(_Analysis)]
@@ -484,9 +485,13 @@ class CostReport:
 
 
 class _DeviceObs:
-    """rgf_obs handle: stencils validated on creation (obs.cpp:18-44)."""
+    """rgf_obs handle: stencils validated on creation (obs.cpp:18-44).
+    `where` is a Grid2D or an operator (its grid and device)."""
 
-    def __init__(self, op: "HorizontalCovarianceOp", obs: ObsSet):
+    def __init__(self, where, obs: ObsSet):
+        op = where if hasattr(where, "grid") else None
+        g = op.grid() if op is not None else where
+        device = int(op.options().device) if op is not None else 0
         pos = np.asarray(obs.positions, dtype=np.float64).reshape(-1, 2)
         vals = np.ascontiguousarray(obs.values, dtype=np.float64).reshape(-1)
         rv = np.ascontiguousarray(obs.r_var, dtype=np.float64).reshape(-1)
@@ -494,9 +499,12 @@ class _DeviceObs:
             raise InvalidArgument("ObsSet: inconsistent column lengths")
         self.n = vals.size
         self._keep = [np.ascontiguousarray(pos[:, 0]), np.ascontiguousarray(pos[:, 1]), vals, rv]
+        m0 = np.ascontiguousarray(np.asarray(g.mask).reshape(-1, g.ny, g.nx)[0], dtype=np.uint8)
+        self._keep.append(m0)
+        desc = _GridDesc(g.nx, g.ny, 1, None, None, _ptr(m0), 0)
         h = _vp()
-        _check(lib.rgf_obs_create(op._h, self.n, *(_ptr(a) for a in self._keep),
-                                  ctypes.byref(h)))
+        _check(lib.rgf_obs_create(ctypes.byref(desc), device, self.n,
+                                  *(_ptr(a) for a in self._keep[:4]), ctypes.byref(h)))
         self._h = h
 
     def __del__(self):
@@ -506,33 +514,38 @@ class _DeviceObs:
             self._h = None
 
 
-def _field2d(op, f):
+def _grid_of(where):
+    return where.grid() if hasattr(where, "grid") else where
+
+
+def _field2d(where, f):
+    g = _grid_of(where)
     f = np.ascontiguousarray(f, dtype=np.float64)
-    if f.size != op.grid().nx * op.grid().ny:
+    if f.size != g.nx * g.ny:
         raise InvalidArgument("field does not match the grid")
-    return f.reshape(op.grid().ny, op.grid().nx)
+    return f.reshape(g.ny, g.nx)
 
 
-def obs_operator(field, obs: ObsSet, op: "HorizontalCovarianceOp") -> np.ndarray:
-    """H: bilinear interpolation at each observation (obs.cpp:59-71)."""
-    f = _field2d(op, field)
-    d = _DeviceObs(op, obs)
+def obs_operator(field, obs: ObsSet, grid) -> np.ndarray:
+    """H: bilinear interpolation at each observation (obs.cpp:59-71).
+    `grid`: the field's Grid2D (or an operator on it)."""
+    f = _field2d(grid, field)
+    d = _DeviceObs(grid, obs)
     out = np.empty(d.n)
     if d.n:
-        _check(lib.rgf_obs_apply(op._h, d._h, 0, _ptr(f), _ptr(out), 0, None))
+        _check(lib.rgf_obs_apply(d._h, 0, _ptr(f), _ptr(out), 0, None))
     return out
 
 
-def obs_operator_transpose(vec, obs: ObsSet, op: "HorizontalCovarianceOp") -> np.ndarray:
+def obs_operator_transpose(vec, obs: ObsSet, grid) -> np.ndarray:
     """H^T: scatter with the same bilinear weights (obs.cpp:73-87)."""
     v = np.ascontiguousarray(vec, dtype=np.float64).reshape(-1)
-    d = _DeviceObs(op, obs)
+    d = _DeviceObs(grid, obs)
     if v.size != d.n:
         raise InvalidArgument("obs_operator_transpose: vector length mismatch")
-    g = op.grid()
+    g = _grid_of(grid)
     out = np.empty((g.ny, g.nx))
-    _check(lib.rgf_obs_apply(op._h, d._h, 1, _ptr(v) if v.size else _ptr(out), _ptr(out), 0,
-                             None))
+    _check(lib.rgf_obs_apply(d._h, 1, _ptr(v) if v.size else _ptr(out), _ptr(out), 0, None))
     return out
 
 

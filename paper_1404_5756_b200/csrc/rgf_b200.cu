@@ -545,6 +545,7 @@ void build_segments(rgf_op* op, const uint8_t* mask_d, int dir, DirData& d) {
 struct rgf_obs {
   int device = 0;
   int64_t n = 0, nx = 0, ny = 0;
+  std::mutex mu;
   std::vector<double> values_h, rvar_h;
   DevBuf<int64_t> cell;
   DevBuf<double4> w;
@@ -559,20 +560,20 @@ namespace {
 
 int blocks_for(int64_t n) { return grid_for(std::max<int64_t>(n, 1), 256, 148 * 8); }
 
-// obs.cpp:18-44
-void obs_stencil(const rgf_op* op, double x, double y, int64_t row, int64_t& i0, int64_t& j0,
+// obs.cpp:18-44 (mask: level 0 of the grid, host)
+void obs_stencil(const rgf_grid_desc* g, double x, double y, int64_t row, int64_t& i0, int64_t& j0,
                  double4& w) {
   const auto fail = [row](const std::string& why) {
     throw InvalidArgument("observation " + std::to_string(row) + ": " + why);
   };
-  if (!std::isfinite(x) || !std::isfinite(y) || x < 0 || y < 0 || x > double(op->nx - 1) ||
-      y > double(op->ny - 1))
+  if (!std::isfinite(x) || !std::isfinite(y) || x < 0 || y < 0 || x > double(g->nx - 1) ||
+      y > double(g->ny - 1))
     fail("position (" + std::to_string(x) + "," + std::to_string(y) + ") is outside the grid");
-  i0 = std::min<int64_t>(static_cast<int64_t>(std::floor(x)), op->nx - 2);
-  j0 = std::min<int64_t>(static_cast<int64_t>(std::floor(y)), op->ny - 2);
+  i0 = std::min<int64_t>(static_cast<int64_t>(std::floor(x)), g->nx - 2);
+  j0 = std::min<int64_t>(static_cast<int64_t>(std::floor(y)), g->ny - 2);
   const double fx = x - double(i0), fy = y - double(j0);
   w = make_double4((1 - fx) * (1 - fy), fx * (1 - fy), (1 - fx) * fy, fx * fy);
-  const auto sea = [&](int64_t i, int64_t j) { return op->mask0[j * op->nx + i] != 0; };
+  const auto sea = [&](int64_t i, int64_t j) { return g->mask[j * g->nx + i] != 0; };
   if (!(sea(i0, j0) || sea(i0 + 1, j0) || sea(i0, j0 + 1) || sea(i0 + 1, j0 + 1)))
     fail("all four stencil corners are land");
 }
@@ -598,14 +599,14 @@ struct Cg {
     double h = 0.0;
     CUDA_OK(cudaMemcpyAsync(&h, scal.p, sizeof(double), cudaMemcpyDeviceToHost, st));
     CUDA_OK(cudaStreamSynchronize(st));
-    op->launches += 2;
+    if (op) op->launches += 2;
     return h;
   }
   void h(const double* f, double* out) {
     if (o->n == 0) return;
     rgfb::k_obs_h<<<blocks_for(o->n), 256, 0, st>>>(f, o->n, o->nx, o->cell.p, o->w.p, out);
     CUDA_OK(cudaGetLastError());
-    op->launches += 1;
+    if (op) op->launches += 1;
   }
   void ht(const double* v, const double* rvar, double* out) {
     CUDA_OK(cudaMemsetAsync(out, 0, static_cast<size_t>(nh) * sizeof(double), st));
@@ -614,7 +615,7 @@ struct Cg {
         v, rvar, o->ncell, o->tcells.p, o->tptr.p, o->tent.p,
         reinterpret_cast<const double*>(o->w.p), out);
     CUDA_OK(cudaGetLastError());
-    op->launches += 1;
+    if (op) op->launches += 1;
   }
   void v(const double* in, double* out) { apply_device<double>(op, RGF_V, in, out, 1, st); }
   // solver.cpp:26-31: V^T H^T (v ./ r_var)
@@ -636,8 +637,10 @@ struct Cg {
   }
 };
 
-void check_cg_op(const rgf_op* op) {
+void check_cg_op(const rgf_op* op, const rgf_obs* o) {
   if (op->nlev != 1) throw InvalidArgument("solve: the operator must have one level");
+  if (o->nx != op->nx || o->ny != op->ny || o->device != op->device)
+    throw InvalidArgument("solve: observations are not on the operator's grid");
 }
 void validate_rvar(const rgf_obs* o) {  // obs.cpp:48-57 (positions checked at creation)
   for (int64_t k = 0; k < o->n; ++k)
@@ -1140,36 +1143,35 @@ int rgf_rf1_apply_1d(const double* in, const double* sigma, int64_t m, int64_t n
 
 
 // ------------------------------------------------------------ observations
-int rgf_obs_create(rgf_op* op, int64_t n, const double* x, const double* y, const double* values,
-                   const double* r_var, rgf_obs** out) {
+int rgf_obs_create(const rgf_grid_desc* grid, int32_t device, int64_t n, const double* x,
+                   const double* y, const double* values, const double* r_var, rgf_obs** out) {
   return guarded([&] {
-    if (!op || !out) throw InvalidArgument("obs: null argument");
+    if (!grid || !grid->mask || !out) throw InvalidArgument("obs: null argument");
+    if (grid->nx < 2 || grid->ny < 2) throw InvalidArgument("obs: grid too small");
     if (n < 0) throw InvalidArgument("ObsSet: inconsistent column lengths");
     if (n > 0 && (!x || !y || !values || !r_var)) throw InvalidArgument("obs: null argument");
     if (n >= (int64_t(1) << 29)) throw InvalidArgument("obs: too many observations");
-    check_cg_op(op);
-    std::lock_guard<std::mutex> lock(op->mu);
-    CUDA_OK(cudaSetDevice(op->device));
+    CUDA_OK(cudaSetDevice(device));
     auto o = std::make_unique<rgf_obs>();
-    o->device = op->device;
+    o->device = device;
     o->n = n;
-    o->nx = op->nx;
-    o->ny = op->ny;
+    o->nx = grid->nx;
+    o->ny = grid->ny;
     std::vector<int64_t> cell(static_cast<size_t>(n));
     std::vector<double4> w(static_cast<size_t>(n));
     for (int64_t k = 0; k < n; ++k) {
       int64_t i0, j0;
-      obs_stencil(op, x[k], y[k], k, i0, j0, w[static_cast<size_t>(k)]);
-      cell[static_cast<size_t>(k)] = j0 * op->nx + i0;
+      obs_stencil(grid, x[k], y[k], k, i0, j0, w[static_cast<size_t>(k)]);
+      cell[static_cast<size_t>(k)] = j0 * grid->nx + i0;
     }
     o->values_h.assign(values, values + n);
     o->rvar_h.assign(r_var, r_var + n);
     // H^T gather lists in observation order (counting sort by cell)
-    const int64_t nh = op->nx * op->ny;
+    const int64_t nh = grid->nx * grid->ny;
     std::vector<int64_t> cnt(static_cast<size_t>(nh) + 1, 0);
     auto corner = [&](int64_t k, int q) {
       const int64_t c = cell[static_cast<size_t>(k)];
-      return c + (q & 1) + (q >> 1) * op->nx;
+      return c + (q & 1) + (q >> 1) * grid->nx;
     };
     for (int64_t k = 0; k < n; ++k)
       for (int q = 0; q < 4; ++q) ++cnt[static_cast<size_t>(corner(k, q)) + 1];
@@ -1213,14 +1215,14 @@ int rgf_obs_destroy(rgf_obs* o) {
 }
 
 // transpose 0: out (n) = H in (ny*nx field); 1: out (field) = H^T in (n)
-int rgf_obs_apply(rgf_op* op, rgf_obs* o, int transpose, const double* in, double* out,
-                  int memory, void* stream) {
+int rgf_obs_apply(rgf_obs* o, int transpose, const double* in, double* out, int memory,
+                  void* stream) {
   return guarded([&] {
-    if (!op || !o || !in || !out) throw InvalidArgument("obs: null argument");
-    std::lock_guard<std::mutex> lock(op->mu);
-    CUDA_OK(cudaSetDevice(op->device));
+    if (!o || !in || !out) throw InvalidArgument("obs: null argument");
+    std::lock_guard<std::mutex> lock(o->mu);
+    CUDA_OK(cudaSetDevice(o->device));
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    Cg cg{op, o, st, op->nx * op->ny, {}, {}, {}, {}, {}};
+    Cg cg{nullptr, o, st, o->nx * o->ny, {}, {}, {}, {}, {}};
     const int64_t nin = transpose ? o->n : cg.nh, nout = transpose ? cg.nh : o->n;
     DevBuf<double> di, dout;
     const double* src = in;
@@ -1250,7 +1252,7 @@ int rgf_cost(rgf_op* op, rgf_obs* o, const double* chi, const double* background
              double* gradient) {
   return guarded([&] {
     if (!op || !o || !chi || !j3 || !gradient) throw InvalidArgument("cost: null argument");
-    check_cg_op(op);
+    check_cg_op(op, o);
     validate_rvar(o);
     std::lock_guard<std::mutex> lock(op->mu);
     CUDA_OK(cudaSetDevice(op->device));
@@ -1291,7 +1293,7 @@ int rgf_solve(rgf_op* op, rgf_obs* o, double tol, int32_t max_iter, const double
     if (!(tol > 0)) throw InvalidArgument("solve: tol must be positive");
     if (max_iter < 0) throw InvalidArgument("solve: max_iter must be >= 0");
     if (!op || !o || !increment || !out || !gnorms) throw InvalidArgument("solve: null argument");
-    check_cg_op(op);
+    check_cg_op(op, o);
     validate_rvar(o);
     std::lock_guard<std::mutex> lock(op->mu);
     CUDA_OK(cudaSetDevice(op->device));

@@ -3,12 +3,14 @@
 // Built and run by tests/test_gpu_facade.py on the GPU box:
 //   g++ -std=c++20 -O2 -I include tests/cpp/test_facade.cpp \
 //       paper_1404_5756_b200/librgf_b200.so -o /tmp/test_facade
+#include <array>
 #include <cmath>
 #include <cstdio>
 #include <random>
 #include <vector>
 
 #include "rgf_b200/covariance.hpp"
+#include "rgf_b200/solver.hpp"
 
 using namespace rgf;
 
@@ -186,6 +188,68 @@ int main() {
     const StateField f = StateField::zeros(other);
     CHECK_THROWS_AS(op.apply_gx(f), std::invalid_argument);
     CHECK_THROWS_AS(op.apply_b(f), std::invalid_argument);
+  }
+  // ---- proj/tests/test_solver.cpp through rgf_b200/solver.hpp
+  auto make_obs = [](std::initializer_list<std::array<double, 4>> rows) {
+    ObsSet o;
+    const Index n = static_cast<Index>(rows.size());
+    o.positions.resize(n, 2);
+    o.values.resize(n);
+    o.r_var.resize(n);
+    Index k = 0;
+    for (const auto& r : rows) {
+      o.positions(k, 0) = r[0];
+      o.positions(k, 1) = r[1];
+      o.values[k] = r[2];
+      o.r_var[k] = r[3];
+      ++k;
+    }
+    return o;
+  };
+  {  // :45-58 exact on affine fields and nodes
+    const Grid2D g = Grid2D::uniform(8, 8, 1000.0, 1000.0);
+    StateField f = StateField::zeros(g);
+    for (Index j = 0; j < 8; ++j)
+      for (Index i = 0; i < 8; ++i) f.values(i, j) = 2.0 * i - 3.0 * j + 1.0;
+    const Vector h = obs_operator(f, make_obs({{3.5, 2.0, 0.0, 1.0}, {5.0, 5.0, 0.0, 1.0}}));
+    CHECK(std::abs(h[0] - (2.0 * 3.5 - 3.0 * 2.0 + 1.0)) <= 1e-14 * 2.0);
+    CHECK(h[1] == f.values(5, 5));
+  }
+  {  // :60-74 rejects all-land stencils and outside positions
+    Grid2D g = Grid2D::uniform(8, 8, 1000.0, 1000.0);
+    g.mask(3, 3) = g.mask(4, 3) = g.mask(3, 4) = g.mask(4, 4) = 0;
+    const StateField f = StateField::zeros(g);
+    CHECK_THROWS_AS(obs_operator(f, make_obs({{3.5, 3.5, 0.0, 1.0}})), std::invalid_argument);
+    CHECK_THROWS_AS(obs_operator(f, make_obs({{-0.5, 2.0, 0.0, 1.0}})), std::invalid_argument);
+  }
+  {  // :165-192 single observation increment
+    const Grid2D g = Grid2D::uniform(64, 64, 6000.0, 6000.0);
+    const HorizontalCovarianceOp op(g, uniform_scale(g, 12000.0));
+    const Analysis an = solve(make_obs({{32, 32, 1.0, 1.0}}), op, {1e-10, 50});
+    CHECK(an.converged);
+    double peak = -1e300;
+    Index imax = -1, jmax = -1;
+    for (Index j = 0; j < 64; ++j)
+      for (Index i = 0; i < 64; ++i)
+        if (an.increment.values(i, j) > peak) {
+          peak = an.increment.values(i, j);
+          imax = i;
+          jmax = j;
+        }
+    CHECK(imax == 32 && jmax == 32);
+    CHECK(peak > 0.0 && peak < 1.0);
+  }
+  {  // :239-250 hitting max_iter flags non-convergence; :139-163 bad options
+    const Grid2D g = Grid2D::uniform(24, 24, 6000.0, 6000.0);
+    const HorizontalCovarianceOp op(g, uniform_scale(g, 12000.0));
+    const Analysis an = solve(
+        make_obs({{5, 5, 1.0, 0.1}, {12, 12, -1.0, 0.1}, {18, 6, 2.0, 0.1}}), op, {1e-15, 1});
+    CHECK(!an.converged);
+    CHECK(an.cg_iterations == 1);
+    CHECK(an.gradient_norms.size() == 2);
+    CHECK_THROWS_AS(solve(make_obs({{6, 6, 1.0, 1.0}}), op, {0.0, 30}), std::invalid_argument);
+    const CostReport r = cost(StateField::zeros(g), make_obs({{3.0, 4.0, 1.0, 0.5}}), op);
+    CHECK(std::abs(r.j_total - 0.5 * 1.0 / 0.5) <= 1e-14);
   }
   std::printf("%d checks, %d failures\n", checks, failures);
   return failures == 0 ? 0 : 1;
