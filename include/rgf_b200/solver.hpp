@@ -12,7 +12,7 @@
 
 namespace rgf {
 
-#ifdef RGF_B200_WITH_EIGEN
+#ifdef RGF_B200_USE_EIGEN
 using Vector = Eigen::VectorXd;
 using Positions = Eigen::ArrayX2d;
 #else

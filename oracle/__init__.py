@@ -157,6 +157,8 @@ class OracleOp:
         self._h = h
 
     def __del__(self):
+        if lib is None:  # interpreter teardown
+            return
         if getattr(self, "_h", None):
             lib.rgfo_op_destroy(self._h)
             self._h = None
@@ -196,6 +198,8 @@ class OracleObs:
         self._h = h
 
     def __del__(self):
+        if lib is None:  # interpreter teardown
+            return
         if getattr(self, "_h", None):
             lib.rgfo_obs_destroy(self._h)
             self._h = None

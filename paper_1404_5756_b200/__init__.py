@@ -234,6 +234,8 @@ class HorizontalCovarianceOp:
         self._h = handle
 
     def __del__(self):
+        if lib is None:  # interpreter teardown
+            return
         h = getattr(self, "_h", None)
         if h:
             lib.rgf_op_destroy(h)
@@ -508,6 +510,8 @@ class _DeviceObs:
         self._h = h
 
     def __del__(self):
+        if lib is None:  # interpreter teardown
+            return
         h = getattr(self, "_h", None)
         if h and lib is not None:
             lib.rgf_obs_destroy(h)

@@ -1,0 +1,58 @@
+"""Measure the device 3D-VAR analysis against the CPU
+oracle on the same problem: a 2-D C3-like grid (one level of the 1442x1021
+tripolar-like config), seeded observations. Prints one JSON line.
+usage: python tools/bench_solve.py [nobs] [max_iter]"""
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import oracle as O  # noqa: E402
+import paper_1404_5756_b200 as P  # noqa: E402
+from paper_1404_5756_b200 import synth  # noqa: E402
+
+nobs = int(sys.argv[1]) if len(sys.argv) > 1 else 20000
+iters = int(sys.argv[2]) if len(sys.argv) > 2 else 30
+cfg = synth.make_config("C3", nlev=1)
+m = cfg.mask[0]
+rng = np.random.default_rng(42)
+pos = np.column_stack([rng.uniform(0, cfg.nx - 1, 4 * nobs), rng.uniform(0, cfg.ny - 1, 4 * nobs)])
+i0 = np.minimum(np.floor(pos[:, 0]).astype(int), cfg.nx - 2)
+j0 = np.minimum(np.floor(pos[:, 1]).astype(int), cfg.ny - 2)
+ok = m[j0, i0] | m[j0, i0 + 1] | m[j0 + 1, i0] | m[j0 + 1, i0 + 1]
+pos = pos[ok][:nobs]
+vals = rng.standard_normal(nobs)
+rv = rng.uniform(0.5, 2.0, nobs)
+grid = P.Grid2D(cfg.nx, cfg.ny, cfg.dx, cfg.dy, cfg.mask)
+op = P.HorizontalCovarianceOp(grid, P.ScaleField(cfg.rx, cfg.ry), P.CovarianceOptions())
+obs = P.ObsSet(pos, vals, rv)
+opts = P.SolveOptions(tol=1e-30, max_iter=iters)  # fixed iteration count
+P.solve(obs, op, P.SolveOptions(tol=1e-30, max_iter=2))  # warm-up
+torch.cuda.synchronize()
+t0 = time.perf_counter()
+an = P.solve(obs, op, opts)
+gpu_s = time.perf_counter() - t0
+threads = os.cpu_count() or 1
+cpu = O.OracleOp(cfg.nx, cfg.ny, cfg.dx, cfg.dy, cfg.mask, cfg.rx, cfg.ry, threads=threads)
+co = O.OracleObs(cpu, pos, vals, rv)
+cit = 3
+t0 = time.perf_counter()
+ref = co.solve(tol=1e-30, max_iter=cit)
+cpu_s = time.perf_counter() - t0
+gpu3 = P.solve(obs, op, P.SolveOptions(tol=1e-30, max_iter=cit))
+rel = float(np.max(np.abs(gpu3.increment - ref["increment"])) / np.max(np.abs(ref["increment"])))
+print(json.dumps({
+    "metric": "3D-VAR CG iteration time (apply_v + H + H^T + apply_v^T + dots)",
+    "grid": f"C3 level 0, {cfg.nx}x{cfg.ny} fp64, 3rd-RF", "nobs": int(nobs),
+    "gpu": {"iterations": an.cg_iterations, "s_total": gpu_s,
+            "ms_per_iteration": 1e3 * gpu_s / max(an.cg_iterations, 1),
+            "timing": "host wall clock around rgf_solve (host arrays in/out)"},
+    "cpu_oracle": {"iterations": cit, "s_total": cpu_s, "ms_per_iteration": 1e3 * cpu_s / cit,
+                   "threads": threads, "kind": "port"},
+    "parity": {"iterations": cit, "increment_rel_max_err": rel},
+}))
