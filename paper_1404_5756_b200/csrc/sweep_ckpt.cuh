@@ -768,7 +768,7 @@ struct YC2 {
 // planes (independent chains interleaved: ILP, and one coefficient load
 // serves PPW chains); results go straight to global memory (coalesced
 // 32-column rows).
-template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S>
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S, int LG>
 __global__ void __launch_bounds__(32 * NW, 1)
     k_yck2(T* __restrict__ out, StreamArgs a, const double* __restrict__ ck,
            const __grid_constant__ CUtensorMap tm_field, const __grid_constant__ CUtensorMap tm_coef,
@@ -776,6 +776,11 @@ __global__ void __launch_bounds__(32 * NW, 1)
   constexpr int NPL = NW * PPW;  // planes per CTA
   using L = YC2<T, NPL>;
   constexpr int X = L::X;
+  // LG > 1: a warp covers 32/LG columns of LG planes (lanes = columns x
+  // planes), so one coefficient load serves LG chains and a warp's
+  // coefficient LDS.128 touches 32/LG distinct 16 B words instead of 32
+  constexpr int CW = 32 / LG;                  // columns per warp
+  static_assert(PPW == 1 || LG == 1, "LG > 1 takes one plane per lane");
   extern __shared__ __align__(16) unsigned char smem_raw[];
   unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * L::bytes);
@@ -789,7 +794,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
   const int64_t ix0 = tile * 32;
   const int ncol = static_cast<int>(nx - ix0 < 32 ? nx - ix0 : 32);
   const int npl = static_cast<int>(planes - p0 < NPL ? planes - p0 : NPL);
-  const int nwp = (npl + PPW - 1) / PPW;
+  const int nwp = LG == 1 ? (npl + PPW - 1) / PPW : ((npl + LG - 1) / LG) * LG;
   const int64_t NB = (ny + X - 1) / X;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -822,8 +827,13 @@ __global__ void __launch_bounds__(32 * NW, 1)
   __syncthreads();
   if (warp >= nwp) return;
 
-  const bool colok = lane < ncol;
-  const int64_t ix = ix0 + (colok ? lane : 0);
+  // this lane's column in the CTA tile and plane slot
+  const int wc = LG == 1 ? 0 : warp % LG;      // column group of the warp
+  const int wp = LG == 1 ? warp : warp / LG;   // plane group of the warp
+  const int cl = LG == 1 ? lane : wc * CW + lane % CW;  // column in the 32-column tile
+  const int ql = LG == 1 ? 0 : lane / CW;      // plane within the warp's group
+  const bool colok = cl < ncol;
+  const int64_t ix = ix0 + (colok ? cl : 0);
   T* dst[PPW];
   const uint64_t* W[PPW];
   const double* PREp[PPW];
@@ -833,7 +843,7 @@ __global__ void __launch_bounds__(32 * NW, 1)
   int64_t pp[PPW];
 #pragma unroll
   for (int c = 0; c < PPW; ++c) {
-    const int pl = warp * PPW + c;
+    const int pl = LG == 1 ? warp * PPW + c : wp * LG + ql;
     act[c] = colok && pl < npl;
     const int64_t p = p0 + (pl < npl ? pl : 0);
     pp[c] = p;
@@ -886,10 +896,11 @@ __global__ void __launch_bounds__(32 * NW, 1)
     }
     mbar_wait(&full[s], static_cast<uint32_t>((bi / S) & 1));
     const unsigned char* base = smem + s * L::bytes;
-    const T* fld = reinterpret_cast<const T*>(base) + warp * PPW * X * 32 + lane;
+    const T* fld = reinterpret_cast<const T*>(base) +
+                   (LG == 1 ? warp * PPW : wp * LG + ql) * X * 32 + cl;
     const double* cs = reinterpret_cast<const double*>(base + L::field);
-    const double* id = reinterpret_cast<const double*>(base + L::field + L::coef) + lane;
-    auto cfu = [&](int uu) -> Coef3 { return coef_soa<X>(cs, uu, lane); };
+    const double* id = reinterpret_cast<const double*>(base + L::field + L::coef) + cl;
+    auto cfu = [&](int uu) -> Coef3 { return coef_soa<X>(cs, uu, cl); };
 
 #pragma unroll
     for (int c = 0; c < PPW; ++c) restore(sa[c], r1[c], r2[c], r3[c]);
@@ -953,7 +964,7 @@ constexpr int kYc1NW = 16, kYc1U = 8, kYc1S = 4;
 template <typename T>
 struct C2Shape {
   static constexpr bool f64 = sizeof(T) == 8;
-  static constexpr int yNW = 12, yPPW = 1, yS = 3;
+  static constexpr int yNW = 12, yPPW = 1, yS = 3, yLG = 1;
   static constexpr int xR = 4, xNWR = 4, xS = 3;
 };
 constexpr int kXc1NW = 4, kXc1S = 4;
@@ -1088,7 +1099,7 @@ void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
   k_yck1<T, TR, IDC, VAR, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(a, ck, tf, tc, ti);
 }
 
-template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S>
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S, int LG = 1>
 void launch_yck2_shape(const T* in, T* out, const StreamArgs& a, const double* ck,
                        cudaStream_t st) {
   constexpr int NPL = NW * PPW;
@@ -1096,7 +1107,7 @@ void launch_yck2_shape(const T* in, T* out, const StreamArgs& a, const double* c
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S>,
+    cudaFuncSetAttribute(k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S, LG>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
@@ -1114,14 +1125,14 @@ void launch_yck2_shape(const T* in, T* out, const StreamArgs& a, const double* c
                                          CU_TENSOR_MAP_SWIZZLE_NONE)
                              : tc;
   const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NPL - 1) / NPL);
-  k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S><<<blocks, 32 * NW, smem, st>>>(out, a, ck, tf, tc,
-                                                                          ti);
+  k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S, LG><<<blocks, 32 * NW, smem, st>>>(out, a, ck, tf,
+                                                                              tc, ti);
 }
 
 template <typename T, bool TR, bool IDC, bool PRE, bool POST>
 void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
-  launch_yck2_shape<T, TR, IDC, PRE, POST, C2Shape<T>::yNW, C2Shape<T>::yPPW, C2Shape<T>::yS>(
-      in, out, a, ck, st);
+  launch_yck2_shape<T, TR, IDC, PRE, POST, C2Shape<T>::yNW, C2Shape<T>::yPPW, C2Shape<T>::yS,
+                    C2Shape<T>::yLG>(in, out, a, ck, st);
 }
 
 // runtime flags -> template flags; returns kernel launches
