@@ -25,6 +25,8 @@
 // two-pass kernels' step for step (FMA order included); the causal state is
 // resumed from its raw form at block starts.
 #pragma once
+#include <cstdlib>
+
 #include "sweep_tma.cuh"
 
 namespace rgfb {
@@ -414,6 +416,137 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
   }
 }
 
+// Paired-stage C1, x (see k_xck1): a stage is two U-point halves fetched as
+// one [32*NW planes][2][U] box, so every (plane, row) is a 256 B run
+template <typename T, bool TR, bool IDC, bool VAR, int NW, int S>
+__global__ void __launch_bounds__(32 * (NW + 1), 1)
+    k_xck1p(StreamArgs a, double* __restrict__ ck, const __grid_constant__ CUtensorMap tm_in,
+           const __grid_constant__ CUtensorMap tm_coef, const __grid_constant__ CUtensorMap tm_idc) {
+  using L = XT<T, NW, false>;
+  constexpr int U = L::U, X = ck_x<T>();
+  static_assert(X == U, "one checkpoint per half stage");
+  constexpr size_t PF = 2 * L::field, PC = 2 * L::coef, PI = 2 * L::idc;
+  constexpr size_t PBYTES = (PF + PC + PI + 1023) / 1024 * 1024;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * PBYTES);
+  uint64_t* empty = full + S;
+
+  const int64_t n = a.nx, ny = a.ny;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
+  const int64_t iy = blockIdx.x / PB;
+  const int64_t p0 = (blockIdx.x - iy * PB) * 32 * NW;
+  const int npl = static_cast<int>(planes - p0 < 32 * NW ? planes - p0 : 32 * NW);
+  const int nwp = (npl + 31) / 32;
+  const int64_t NB = (n + X - 1) / X;
+  const int64_t nst = NB / 2;  // paired stages covering blocks 0..NB-2 (checkpoints 1..NB-1)
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], nwp);
+    }
+    mbar_fence_init();
+  }
+  __syncthreads();
+
+  if (warp == NW) {  // producer
+    if (lane == 0) {
+      const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+      tma_prefetch_desc(&tm_in);
+      tma_prefetch_desc(&tm_coef);
+      const uint32_t total = static_cast<uint32_t>(PF + PC + (IDC ? PI : 0));
+      for (int64_t i = 0; i < nst; ++i) {
+        const int s = static_cast<int>(i % S);
+        const int64_t m = i / S;
+        if (m > 0) mbar_wait(&empty[s], static_cast<uint32_t>((m - 1) & 1));
+        const int k0 = static_cast<int>(i * 2 * U);
+        unsigned char* base = smem + s * PBYTES;
+        mbar_arrive_expect_tx(&full[s], total);
+        tma_load_4d(base, &tm_in, 0, static_cast<int>(2 * i), static_cast<int>(iy),
+                    static_cast<int>(p0), &full[s], pol_stream);
+        tma_load_2d(base + PF, &tm_coef, 4 * k0, static_cast<int>(iy), &full[s], pol_keep);
+        if constexpr (IDC)
+          tma_load_2d(base + PF + PC, &tm_idc, k0, static_cast<int>(iy), &full[s], pol_keep);
+      }
+    }
+    return;
+  }
+  if (warp >= nwp) return;
+
+  const int pr = warp * 32 + lane;
+  const bool act = pr < npl;
+  const int64_t p = p0 + (act ? pr : 0);
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
+  // transposed mask words: lanes (consecutive levels) read consecutive words
+  const uint64_t* W = a.bitsT + iy * a.words * a.nlev_all + lev;
+  const int64_t ws = a.nlev_all;
+  const double* PRE = VAR ? a.pre_scale + lev * n * ny + iy * n : nullptr;
+  WordStream sbw;
+  sbw.start(W, ws, a.words);
+  typename std::conditional<TR, AdjA2, FwdA2>::type st;
+  uint32_t carry = 0;
+  constexpr int EPC = 16 / int(sizeof(T));
+  const int sw = pr & 7;
+
+  for (int64_t i = 0; i < nst; ++i) {
+    const int s = static_cast<int>(i % S);
+    mbar_wait(&full[s], static_cast<uint32_t>((i / S) & 1));
+    const unsigned char* base = smem + s * PBYTES;
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int64_t k0 = (2 * i + h) * U;
+      sbw.advance(W, ws, a.words, k0);
+      const uint32_t sb = sbw.stage<U>(k0);
+      const uint32_t starts = sb & ~((sb << 1) | carry);
+      const Coef3* cf = reinterpret_cast<const Coef3*>(base + PF) + h * U;
+      const double* id = reinterpret_cast<const double*>(base + PF + PC) + h * U;
+      const int rr = pr * 2 + h;
+      const unsigned char* rowp = base + rr * 128;
+      const int sw = rr & 7;
+#pragma unroll 1
+      for (int q = 0; q < U / EPC; ++q) {
+        const void* cp = rowp + ((q ^ sw) << 4);
+        double v[EPC];
+        if constexpr (sizeof(T) == 8) {
+          const double2 t = *reinterpret_cast<const double2*>(cp);
+          v[0] = t.x;
+          v[1] = t.y;
+        } else {
+          const float4 t = *reinterpret_cast<const float4*>(cp);
+          v[0] = t.x;
+          v[1] = t.y;
+          v[2] = t.z;
+          v[3] = t.w;
+        }
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const int u = q * EPC + e;
+          if ((starts >> u) & 1u) st.reset();
+          double w = v[e];
+          if constexpr (TR && VAR) w *= __ldg(PRE + k0 + u);
+          if constexpr (TR && IDC) w *= id[u];
+          st.step(cf[u], w);
+        }
+      }
+      carry = (sb >> (U - 1)) & 1u;
+      const int64_t b = 2 * i + h + 1;  // raw state entering block b
+      if (act && b < NB) {
+        const double4 r = st.raw();
+        double* o = ck + ((iy * NB + b) * 3) * planes + p;
+        __stcg(o, r.x);
+        __stcg(o + planes, r.y);
+        __stcg(o + 2 * planes, r.z);
+      }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[s]);
+  }
+}
+
+
 // C2, x layout: R rows x 32*NWR planes per CTA; a block is NS subtiles of
 // [R rows][32*NWR planes][128 B], 128 B swizzled (the tensor map lists the
 // plane dimension before the row dimension, so a warp's 32 planes are 32
@@ -633,6 +766,221 @@ __global__ void __launch_bounds__(32 * R * NWR, 1)
     bulk_wait_all();
   }
 }
+
+// Paired-tile variant of C2, x layout (see k_xck2)
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int R, int NWR, int S>
+__global__ void __launch_bounds__(32 * R * NWR, 1)
+    k_xck2p(StreamArgs a, const double* __restrict__ ck, const __grid_constant__ CUtensorMap tm_in,
+           const __grid_constant__ CUtensorMap tm_out, const __grid_constant__ CUtensorMap tm_coef,
+           const __grid_constant__ CUtensorMap tm_idc) {
+  using L = XC2<T, R, NWR>;
+  constexpr int U = L::U, X = L::X, NWC = R * NWR;
+  static_assert(L::NS == 1, "paired tiles take one 128 B subtile per block");
+  // a tile is two consecutive blocks: [R rows][32*NWR planes][2][X], so every
+  // (plane, row) is fetched and stored as one 256 B run (a TMA copy with
+  // 128 B runs caps at ~4.9 TB/s, with 256 B runs at ~6.2 TB/s:
+  // tools/probe/tma_copy_probe.cu)
+  constexpr size_t TF = 2 * L::sub, TC = 2 * L::coef, TI = 2 * L::idc;
+  constexpr size_t TB = (TF + TC + TI + 1023) / 1024 * 1024;
+  constexpr int ESZ = static_cast<int>(sizeof(T));
+  constexpr int EPC = 16 / ESZ;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + S * TB);
+  int* released = reinterpret_cast<int*>(full + S);  // warps done with a buffer
+
+  const int64_t n = a.nx, ny = a.ny, nh = n * ny;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t PB = (planes + 32 * NWR - 1) / (32 * NWR);
+  const int64_t iyb = blockIdx.x / PB;
+  const int64_t p0 = (blockIdx.x - iyb * PB) * 32 * NWR;
+  const int64_t iy0 = iyb * R;
+  const int npl = static_cast<int>(planes - p0 < 32 * NWR ? planes - p0 : 32 * NWR);
+  const int64_t NB = (n + X - 1) / X;
+  const int64_t NT = (NB + 1) / 2;  // tiles
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  // No producer warp and no CTA-wide barrier: each warp returns its own
+  // [32 planes x 1 row] part of a block with a TMA store, and the last warp
+  // to release a buffer (its store read out) issues the buffer's next load.
+  auto load_tile = [&](int64_t ti) {
+    const int s = static_cast<int>(ti % S);
+    const int64_t j = NT - 1 - ti;  // blocks 2j, 2j+1
+    unsigned char* base = smem + s * TB;
+    const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
+    mbar_arrive_expect_tx(&full[s], static_cast<uint32_t>(TF + TC + (IDC ? TI : 0)));
+    tma_load_4d(base, &tm_in, 0, static_cast<int>(2 * j), static_cast<int>(p0), static_cast<int>(iy0),
+                &full[s], pol_stream);
+    tma_load_2d(base + TF, &tm_coef, static_cast<int>(4 * 2 * j * X), static_cast<int>(iy0),
+                &full[s], pol_keep);
+    if constexpr (IDC)
+      tma_load_2d(base + TF + TC, &tm_idc, static_cast<int>(2 * j * X), static_cast<int>(iy0),
+                  &full[s], pol_keep);
+  };
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      released[s] = 0;
+    }
+    mbar_fence_init();
+    tma_prefetch_desc(&tm_in);
+    tma_prefetch_desc(&tm_coef);
+    for (int64_t ti = 0; ti < S && ti < NT; ++ti) load_tile(ti);
+  }
+  __syncthreads();
+  // lane 0 of each warp: once this warp's store of block `bi` has read its
+  // buffer, count the warp out; the last one refills the buffer
+  auto release = [&](int64_t ti) {
+    asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");
+    const int s = static_cast<int>(ti % S);
+    if (atomicAdd(&released[s], 1) == NWC - 1) {
+      released[s] = 0;
+      if (ti + S < NT) load_tile(ti + S);
+    }
+  };
+
+  // consumers: warp -> (row r, 32 planes)
+  const int r = warp / NWR;
+  const int pg = warp - r * NWR;
+  const int pl = pg * 32 + lane;
+  const int64_t iy = iy0 + r;
+  const bool act = pl < npl && iy < ny;
+  const int64_t p = p0 + (pl < npl ? pl : 0);
+  const int64_t iyc = iy < ny ? iy : iy0;
+  const int64_t var = p / a.nlev, lev = a.lev0 + (p - var * a.nlev);
+  (void)var;
+  const uint64_t* W = a.bitsT + iyc * a.words * a.nlev_all + lev;
+  const int64_t ws = a.nlev_all;
+  const double* PREp = PRE ? a.pre_scale + lev * nh + iyc * n : nullptr;
+  const double* POSTp = POST ? a.post_scale + lev * nh + iyc * n : nullptr;
+  const double* Mrow = a.clos + clos_off(a.cls[lev], 0, TR ? 1 : 0, nh, iyc * n);
+  const bool ghosts = a.ghost[lev] > 0;
+  const int rs0 = (r * 32 * NWR + pl) * 2;  // 128 B row of this chain's first block
+  typename std::conditional<TR, AdjA2, FwdA2>::type sa;
+  typename std::conditional<TR, AdjD2, FwdD2>::type sd;
+  auto meta = [&](int64_t b) {
+    return load_meta<X>(ck + ((iy * NB + b) * 3) * planes + p, b > 0 && act, planes, W, ws,
+                        b * X, a.words);
+  };
+  BlockMeta next = meta(NB - 1);
+
+  for (int64_t bi = 0; bi < NB; ++bi) {
+    const int64_t b = NB - 1 - bi;
+    const int64_t kb = b * X;
+    const int h = static_cast<int>(b & 1);
+    const int64_t ti = NT - 1 - (b >> 1);
+    const int s = static_cast<int>(ti % S);
+    const bool tile_first = h == 1 || bi == 0;
+    const int rs = rs0 + h;
+    const int sw = rs & 7;
+    const BlockMeta cur = next;
+    if (b > 0) next = meta(b - 1);  // consumed one block from now
+    const double r1 = cur.r1, r2 = cur.r2, r3 = cur.r3;
+    const BlockBits bb = decode_bits<X>(cur, kb, a.words);
+    const uint32_t sb = bb.sb, sm1 = bb.sm1, sm2 = bb.sm2, after = bb.after;
+    const uint32_t starts = sb & ~((sb << 1) | sm1);
+    const uint32_t ends = sb & ~((sb >> 1) | (after << (X - 1)));
+    const int jl = first_end(ends);
+    const Closure mpre = prefetch_closure(Mrow + (kb + (jl > 0 ? jl : 0)) * 10,
+                                          jl >= 0 && kb + jl < n - 1 && ghosts);
+    if (tile_first) mbar_wait(&full[s], static_cast<uint32_t>((ti / S) & 1));
+    unsigned char* base = smem + s * TB;
+    const Coef3* cf = reinterpret_cast<const Coef3*>(base + TF) + r * 2 * X + h * X;
+    const double* id = reinterpret_cast<const double*>(base + TF + TC) + r * 2 * X + h * X;
+    auto cfu = [&](int uu) -> Coef3 { return lds_coef(cf + uu); };
+
+    // ---- causal recursion over the block from its checkpoint (registers)
+    restore(sa, r1, r2, r3);
+    double pv[X];
+#pragma unroll
+    for (int t = 0; t < 1; ++t) {
+      const unsigned char* rowp = base + rs * 128;
+#pragma unroll
+      for (int q = 0; q < U / EPC; ++q) {
+        const void* cp = rowp + ((q ^ sw) << 4);
+        double v[EPC];
+        if constexpr (sizeof(T) == 8) {
+          const double2 tv = *reinterpret_cast<const double2*>(cp);
+          v[0] = tv.x;
+          v[1] = tv.y;
+        } else {
+          const float4 tv = *reinterpret_cast<const float4*>(cp);
+          v[0] = tv.x;
+          v[1] = tv.y;
+          v[2] = tv.z;
+          v[3] = tv.w;
+        }
+#pragma unroll
+        for (int e = 0; e < EPC; ++e) {
+          const int u = q * EPC + e;
+          reset_if(sa, (starts >> u) & 1u);
+          double w = v[e];
+          if constexpr (TR && PRE) w *= __ldg(PREp + kb + u);
+          if constexpr (TR && IDC) w *= id[u];
+          pv[u] = sa.step(cfu(u), w);
+        }
+      }
+    }
+    // the previous tile's store has had the whole causal pass to read out
+    if (lane == 0 && tile_first && ti >= 1) release(ti - 1);
+
+    // ---- anti-causal recursion down the block, results in place
+#pragma unroll
+    for (int t = 0; t >= 0; --t) {
+      unsigned char* rowp = base + rs * 128;
+#pragma unroll
+      for (int q = U / EPC - 1; q >= 0; --q) {
+        void* cp = rowp + ((q ^ sw) << 4);
+        double o[EPC];
+#pragma unroll
+        for (int e = EPC - 1; e >= 0; --e) {
+          const int u = q * EPC + e;
+          const Coef3 c = cfu(u);
+          if ((ends >> u) & 1u) {  // segment end: enter from the right ghosts
+            if (kb + u < n - 1 && ghosts) {
+              const bool s1 = u >= 1 ? ((sb >> (u >= 1 ? u - 1 : 0)) & 1u) : sm1;
+              const bool s2 =
+                  s1 && (u >= 2 ? ((sb >> (u >= 2 ? u - 2 : 0)) & 1u) : (u == 1 ? sm1 : sm2));
+              const Closure M = u == jl ? mpre : load_closure(Mrow + (kb + u) * 10);
+              enter(sd, segment_entry<TR, X>(pv, u, r1, r2, r3, s1, s2, c, cfu, M), c);
+            } else {
+              sd.reset();
+            }
+          }
+          double ov = sd.step(c, c.b * pv[u]);
+          if constexpr (!TR && IDC) ov *= id[u];
+          if constexpr (POST) ov *= __ldg(POSTp + kb + u);
+          o[e] = ((sb >> u) & 1u) ? ov : 0.0;
+        }
+        if constexpr (sizeof(T) == 8) {
+          *reinterpret_cast<double2*>(cp) = make_double2(o[0], o[1]);
+        } else {
+          *reinterpret_cast<float4*>(cp) =
+              make_float4(static_cast<float>(o[0]), static_cast<float>(o[1]),
+                          static_cast<float>(o[2]), static_cast<float>(o[3]));
+        }
+      }
+    }
+    // tile done (its lower block): this warp's [32 planes x 1 row x 2 blocks]
+    // back to global memory as 256 B runs
+    if (h == 0) {
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) {
+        if (iy < ny && pg * 32 < npl)
+          tma_store_4d(&tm_out, 0, static_cast<int>(2 * (b >> 1)), static_cast<int>(p0 + pg * 32),
+                       static_cast<int>(iy), base + ((r * 32 * NWR + pg * 32) * 2) * 128,
+                       l2_evict_first());
+        bulk_commit();
+      }
+    }
+  }
+  if (lane == 0) {
+    if (NT >= 1) release(NT - 1);
+    bulk_wait_all();
+  }
+}
+
 
 // ============================================================ y-sweep
 // Coefficients of the y direction in SoA rows [ny][4][nx] (a1, a2, a3, b):
@@ -966,6 +1314,7 @@ struct C2Shape {
   static constexpr bool f64 = sizeof(T) == 8;
   static constexpr int yNW = 12, yPPW = 1, yS = 3, yLG = 1;
   static constexpr int xR = 4, xNWR = 4, xS = 3;
+  static constexpr int pR = 3, pNWR = 4, pS = 2;  // paired x tiles: 98 KB each
 };
 constexpr int kXc1NW = 4, kXc1S = 4;
 
@@ -1010,8 +1359,51 @@ void launch_xck1_shape(const T* in, const StreamArgs& a, double* ck, cudaStream_
   k_xck1<T, TR, IDC, VAR, NW, S><<<a.ny * PB, 32 * (NW + 1), smem, st>>>(a, ck, tin, tc, ti);
 }
 
+template <typename T, bool TR, bool IDC, bool VAR, int NW, int S>
+void launch_xck1p_shape(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) {
+  using L = XT<T, NW, false>;
+  constexpr int U = L::U;
+  constexpr size_t PBYTES = (2 * (L::field + L::coef + L::idc) + 1023) / 1024 * 1024;
+  const size_t smem = S * PBYTES + 2 * S * sizeof(uint64_t) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_xck1p<T, TR, IDC, VAR, NW, S>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  const int64_t planes = a.nvar * a.nlev;
+  const uint64_t sz = sizeof(T);
+  // dims (x within a block, block, row, plane): stages land as [plane][2][U]
+  const uint64_t fd[4] = {uint64_t(U), uint64_t(a.nx / U), uint64_t(a.ny), uint64_t(planes)};
+  const uint64_t fs[3] = {uint64_t(U) * sz, uint64_t(a.pitch) * sz, uint64_t(a.pitch * a.ny) * sz};
+  const uint32_t fb[4] = {uint32_t(U), 2, 1, uint32_t(32 * NW)};
+  const CUtensorMap tin = make_tmap(in, tma_dtype<T>(), 4, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  const uint64_t cd[2] = {uint64_t(4 * a.nx), uint64_t(a.ny)};
+  const uint64_t cs[1] = {uint64_t(4 * a.nx) * 8};
+  const uint32_t cb[2] = {uint32_t(4 * 2 * U), 1};
+  const CUtensorMap tc =
+      make_tmap(a.c3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
+  const uint64_t is[1] = {uint64_t(a.ipitch) * 8};
+  const uint32_t ib[2] = {uint32_t(2 * U), 1};
+  const CUtensorMap ti = IDC ? make_tmap(a.idcp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+                                         CU_TENSOR_MAP_SWIZZLE_NONE)
+                             : tc;
+  const int64_t PB = (planes + 32 * NW - 1) / (32 * NW);
+  k_xck1p<T, TR, IDC, VAR, NW, S><<<a.ny * PB, 32 * (NW + 1), smem, st>>>(a, ck, tin, tc, ti);
+}
+
 template <typename T, bool TR, bool IDC, bool VAR>
 void launch_xck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) {
+  static const bool pair_env = [] {
+    const char* e = std::getenv("RGF_B200_XPAIR");
+    return !(e && e[0] == '0');
+  }();
+  if (pair_env && a.nx % ck_x<T>() == 0) {  // paired stages: 256 B runs
+    launch_xck1p_shape<T, TR, IDC, VAR, kXc1NW, 2>(in, a, ck, st);
+    return;
+  }
   // 4 stages, 3 CTAs/SM (1.75 ms on C5 fp64; 6 stages 1.90, 8 or 12 stages
   // at 1 CTA/SM ~3 ms)
   launch_xck1_shape<T, TR, IDC, VAR, kXc1NW, kXc1S>(in, a, ck, st);
@@ -1056,8 +1448,59 @@ void launch_xck2_shape(const T* in, T* out, const StreamArgs& a, const double* c
                                                                                tc, ti);
 }
 
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int R, int NWR, int S>
+void launch_xck2p_shape(const T* in, T* out, const StreamArgs& a, const double* ck,
+                        cudaStream_t st) {
+  using L = XC2<T, R, NWR>;
+  constexpr int X = L::X;
+  constexpr size_t TB = (2 * (L::sub + L::coef + L::idc) + 1023) / 1024 * 1024;
+  const size_t smem = S * TB + 2 * S * sizeof(uint64_t) + 1024;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_xck2p<T, TR, IDC, PRE, POST, R, NWR, S>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    attr = true;
+  }
+  const int64_t planes = a.nvar * a.nlev;
+  const uint64_t sz = sizeof(T);
+  // dims (x within a block, block, plane, row): tiles land as [row][plane][2][X]
+  const uint64_t fd[4] = {uint64_t(X), uint64_t(a.nx / X), uint64_t(planes), uint64_t(a.ny)};
+  const uint64_t fs[3] = {uint64_t(X) * sz, uint64_t(a.pitch * a.ny) * sz, uint64_t(a.pitch) * sz};
+  const uint32_t fb[4] = {uint32_t(X), 2, uint32_t(32 * NWR), uint32_t(R)};
+  const CUtensorMap tin = make_tmap(in, tma_dtype<T>(), 4, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_128B,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  const uint32_t fbo[4] = {uint32_t(X), 2, 32, 1};  // one warp's part
+  const CUtensorMap tout = make_tmap(out, tma_dtype<T>(), 4, fd, fs, fbo,
+                                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  const uint64_t cd[2] = {uint64_t(4 * a.nx), uint64_t(a.ny)};
+  const uint64_t cs[1] = {uint64_t(4 * a.nx) * 8};
+  const uint32_t cb[2] = {uint32_t(4 * 2 * X), uint32_t(R)};
+  const CUtensorMap tc =
+      make_tmap(a.c3, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, cd, cs, cb, CU_TENSOR_MAP_SWIZZLE_NONE);
+  const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
+  const uint64_t is[1] = {uint64_t(a.ipitch) * 8};
+  const uint32_t ib[2] = {uint32_t(2 * X), uint32_t(R)};
+  const CUtensorMap ti = IDC ? make_tmap(a.idcp, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, id, is, ib,
+                                         CU_TENSOR_MAP_SWIZZLE_NONE)
+                             : tc;
+  const int64_t PB = (planes + 32 * NWR - 1) / (32 * NWR);
+  const int64_t blocks = ((a.ny + R - 1) / R) * PB;
+  k_xck2p<T, TR, IDC, PRE, POST, R, NWR, S><<<blocks, 32 * R * NWR, smem, st>>>(a, ck, tin, tout,
+                                                                                tc, ti);
+}
+
 template <typename T, bool TR, bool IDC, bool PRE, bool POST>
 void launch_xck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
+  // rows whole blocks long: paired tiles (256 B runs), unless RGF_B200_XPAIR=0
+  static const bool pair_env = [] {
+    const char* e = std::getenv("RGF_B200_XPAIR");
+    return !(e && e[0] == '0');
+  }();
+  if (pair_env && a.nx % ck_x<T>() == 0) {
+    launch_xck2p_shape<T, TR, IDC, PRE, POST, C2Shape<T>::pR, C2Shape<T>::pNWR, C2Shape<T>::pS>(
+        in, out, a, ck, st);
+    return;
+  }
   launch_xck2_shape<T, TR, IDC, PRE, POST, C2Shape<T>::xR, C2Shape<T>::xNWR, C2Shape<T>::xS>(
       in, out, a, ck, st);
 }
