@@ -67,7 +67,7 @@ def test_all_kinds_fp64_random_masks(P, order, k, nx):
         assert np.all(got[:, land] == 0.0), name
 
 
-@pytest.mark.parametrize("order,k,nx", [(3, 1, 57), (3, 1, 60), (1, 5, 57)])
+@pytest.mark.parametrize("order,k,nx", [(3, 1, 57), (3, 1, 60), (1, 5, 57), (3, 1, 96), (3, 1, 160)])
 def test_fp32_storage(P, order, k, nx):
     g, rx, ry = random_case(40 + order, nx=nx)
     gpu, cpu = build_pair(P, g, rx, ry, order=order, k=k)
@@ -505,4 +505,27 @@ def test_rf1_line_resident_matches_streaming(P, monkeypatch, k, nx, ny, sea, dt)
         assert np.array_equal(got, ref), (name, relmax(got, ref))
         want = cpu.apply(getattr(O, name), f.astype(np.float64))
         assert relmax(got, want) <= (TOL64 if dt == "f64" else TOL32), (name, relmax(got, want))
+        assert np.all(got[:, ~g["mask"]] == 0.0), name
+
+
+
+@pytest.mark.parametrize("nx,dt", [(96, "f64"), (160, "f32"), (64, "f64")])
+def test_paired_x_tiles_match_single(P, monkeypatch, nx, dt):
+    """Rows a whole number of blocks long take the paired x tiles (256 B
+    runs, k_xck1p/k_xck2p); RGF_B200_XPAIR=0 (read at first launch) is not
+    switchable inside one process, so compare against the oracle and check
+    every kind, with variance and per-level masks; nx = 96 gives an odd
+    block count (6 blocks of 16 -> 3 tiles; 160 fp32 -> 5 blocks of 32)."""
+    g, rx, ry = random_case(950 + nx, nx=nx, ny=41, nlev=4, sea=0.7)
+    var = np.random.default_rng(23).uniform(0.5, 2.0, (4, 41, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
+    f = np.random.default_rng(24).standard_normal((2, 4, 41, nx))
+    tol = TOL64
+    if dt == "f32":
+        f = f.astype(np.float32)
+        tol = TOL32
+    for name in KINDS:
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f.astype(np.float64))
+        assert relmax(got, want) <= tol, (name, relmax(got, want))
         assert np.all(got[:, ~g["mask"]] == 0.0), name
