@@ -529,3 +529,23 @@ def test_paired_x_tiles_match_single(P, monkeypatch, nx, dt):
         want = cpu.apply(getattr(O, name), f.astype(np.float64))
         assert relmax(got, want) <= tol, (name, relmax(got, want))
         assert np.all(got[:, ~g["mask"]] == 0.0), name
+
+
+
+@pytest.mark.parametrize("nx,dt", [(80, "f64"), (96, "f64"), (96, "f32")])
+def test_rf1_block_multiple_rows(P, nx, dt):
+    """1st-RF streaming passes on rows a whole number of 128 B blocks long,
+    odd and even block counts, fp64 and fp32, every kind with variance."""
+    g, rx, ry = random_case(970 + nx, nx=nx, ny=33, nlev=3, sea=0.65)
+    var = np.random.default_rng(25).uniform(0.5, 2.0, (3, 33, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, order=1, k=5, variance=var)
+    f = np.random.default_rng(26).standard_normal((2, 3, 33, nx))
+    tol = TOL64
+    if dt == "f32":
+        f = f.astype(np.float32)
+        tol = TOL32
+    for name in KINDS:
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f.astype(np.float64))
+        assert relmax(got, want) <= tol, (name, relmax(got, want))
+        assert np.all(got[:, ~g["mask"]] == 0.0), name
