@@ -122,20 +122,6 @@ __device__ __forceinline__ void ring_st(unsigned char* fs, int lane, const doubl
   }
 }
 
-// wait until at most n (clamped to 7) committed bulk stores may still read smem
-__device__ __forceinline__ void bulk_wait_read_upto(int n) {
-  switch (n < 7 ? n : 7) {
-    case 0: asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); break;
-    case 1: asm volatile("cp.async.bulk.wait_group.read 1;\n" ::: "memory"); break;
-    case 2: asm volatile("cp.async.bulk.wait_group.read 2;\n" ::: "memory"); break;
-    case 3: asm volatile("cp.async.bulk.wait_group.read 3;\n" ::: "memory"); break;
-    case 4: asm volatile("cp.async.bulk.wait_group.read 4;\n" ::: "memory"); break;
-    case 5: asm volatile("cp.async.bulk.wait_group.read 5;\n" ::: "memory"); break;
-    case 6: asm volatile("cp.async.bulk.wait_group.read 6;\n" ::: "memory"); break;
-    default: asm volatile("cp.async.bulk.wait_group.read 7;\n" ::: "memory"); break;
-  }
-}
-
 // block bits of one lane: sea bits, starts, ends (+ the two bits before)
 struct RingBits {
   uint32_t sb, sm1, sm2, after;
