@@ -1117,7 +1117,7 @@ struct YC2 {
 // serves PPW chains); results go straight to global memory (coalesced
 // 32-column rows).
 template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S, int LG>
-__global__ void __launch_bounds__(32 * NW, 1)
+__global__ void __launch_bounds__(32 * NW, NW <= 8 ? 2 : 1)
     k_yck2(T* __restrict__ out, StreamArgs a, const double* __restrict__ ck,
            const __grid_constant__ CUtensorMap tm_field, const __grid_constant__ CUtensorMap tm_coef,
            const __grid_constant__ CUtensorMap tm_idc) {
@@ -1312,7 +1312,7 @@ constexpr int kYc1NW = 16, kYc1U = 8, kYc1S = 4;
 template <typename T>
 struct C2Shape {
   static constexpr bool f64 = sizeof(T) == 8;
-  static constexpr int yNW = 12, yPPW = 1, yS = 3, yLG = 1;
+  static constexpr int yNW = 8, yPPW = 1, yS = 2, yLG = 1;
   static constexpr int xR = 4, xNWR = 4, xS = 3;
   static constexpr int pR = 3, pNWR = 4, pS = 2;  // paired x tiles: 98 KB each
 };
