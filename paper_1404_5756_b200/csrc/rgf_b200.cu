@@ -151,6 +151,14 @@ struct rgf_op {
   int64_t words[2] = {0, 0};
   DevBuf<int> cls_d;
   DevBuf<double> clos;  // [class][dir][nh][18]
+  std::vector<int64_t> class_g;  // ghost width of each closure class
+  // Few-plane x sweeps run as y sweeps on the transposed field (lanes = rows
+  // instead of planes): the x tables in the transposed frame, built on first use
+  bool xt_ok = false;
+  DevBuf<rgfb::Coef3> xt_c3;
+  DevBuf<double> xt_c3s, xt_idc, xt_clos;
+  DevBuf<uint64_t> xt_bitsT;
+  DevBuf<char> xt_in, xt_out;
   DevBuf<double4> entry;  // [var][segments] anti-causal entry states (apply scratch)
   int nclass = 0;
   // host-apply pipeline: H2D / compute / D2H streams, per-slot chunk buffers
@@ -196,6 +204,74 @@ int64_t field_pitch(const rgf_op* op) {
   return (op->nx + q - 1) / q * q;
 }
 
+// out[p][x][y] = in[p][y][x] (in rows `pin` apart, out rows `pout` apart)
+template <typename T>
+__global__ void k_transpose_planes(const T* __restrict__ in, T* __restrict__ out, int64_t nx,
+                                   int64_t ny, int64_t pin, int64_t pout, int64_t planes) {
+  __shared__ T tile[32][33];
+  const int64_t tx = (nx + 31) / 32, ty = (ny + 31) / 32;
+  for (int64_t t = blockIdx.x; t < planes * tx * ty; t += gridDim.x) {
+    const int64_t p = t / (tx * ty), r = t - p * tx * ty;
+    const int64_t by = r / tx, bx = r - by * tx;
+    const T* src = in + p * ny * pin;
+    T* dst = out + p * nx * pout;
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+      const int64_t y = by * 32 + j, x = bx * 32 + threadIdx.x;
+      if (y < ny && x < nx) tile[j][threadIdx.x] = src[y * pin + x];
+    }
+    __syncthreads();
+    for (int j = threadIdx.y; j < 32; j += blockDim.y) {
+      const int64_t x = bx * 32 + j, y = by * 32 + threadIdx.x;
+      if (y < ny && x < nx) dst[x * pout + y] = tile[threadIdx.x][j];
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+void transpose_planes(const T* in, T* out, int64_t nx, int64_t ny, int64_t pin, int64_t pout,
+                      int64_t planes, cudaStream_t st) {
+  const int64_t tiles = planes * ((nx + 31) / 32) * ((ny + 31) / 32);
+  const int blocks = static_cast<int>(std::min<int64_t>(tiles, 148 * 16));
+  k_transpose_planes<T><<<blocks, dim3(32, 8), 0, st>>>(in, out, nx, ny, pin, pout, planes);
+  CUDA_OK(cudaGetLastError());
+}
+
+// x tables in the transposed frame (x runs down the rows of a [nx][ny] field)
+void build_xt(rgf_op* op, cudaStream_t st) {
+  const int64_t nx = op->nx, ny = op->ny, nh = nx * ny;
+  op->xt_c3.alloc(static_cast<size_t>(nh));
+  transpose_planes<rgfb::Coef3>(op->dx_.c3.p, op->xt_c3.p, nx, ny, nx, ny, 1, st);
+  op->xt_c3s.alloc(static_cast<size_t>(4 * nh));
+  rgfb::k_coef_soa<<<grid_for(nh, 256), 256, 0, st>>>(op->xt_c3.p, ny, nx, op->xt_c3s.p);
+  CUDA_OK(cudaGetLastError());
+  if (op->unit_dc) {  // rows padded to an even count (TMA: 16 B row pitch)
+    const int64_t ip = (ny + 1) / 2 * 2;
+    op->xt_idc.alloc(static_cast<size_t>(nx * ip));
+    transpose_planes<double>(op->dx_.idc.p, op->xt_idc.p, nx, ny, nx, ip, 1, st);
+  }
+  // x bits [lev][iy][word] -> y-style chain-minor [lev][word][iy]
+  const int64_t tot = op->nlev * ny * op->words[0];
+  op->xt_bitsT.alloc(static_cast<size_t>(tot));
+  rgfb::k_bits_transpose<<<grid_for(tot, 256), 256, 0, st>>>(op->bits[0].p, 1, ny, nx, op->nlev,
+                                                             op->words[0], op->xt_bitsT.p);
+  CUDA_OK(cudaGetLastError());
+  op->xt_clos.alloc(static_cast<size_t>(op->nclass) * 2 * 2 * nh * 10);
+  const int threads = 128;
+  const int blocks = grid_for(nh, threads, 148 * 8);
+  const int64_t slab = op->gmax + 1;
+  DevBuf<double> scr;
+  scr.alloc(static_cast<size_t>(blocks) * threads * slab);
+  for (int c = 0; c < op->nclass; ++c) {
+    rgfb::k_closures<<<blocks, threads, 0, st>>>(op->xt_c3.p, nh, static_cast<int>(op->class_g[c]),
+                                                 op->xt_clos.p + rgfb::clos_off(c, 1, 0, nh, 0),
+                                                 scr.p, slab);
+    CUDA_OK(cudaGetLastError());
+  }
+  CUDA_OK(cudaStreamSynchronize(st));
+  op->xt_ok = true;
+}
+
 template <typename T>
 void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nvar,
            int64_t lev0, int64_t nlev, const double* pre, const double* post, cudaStream_t st,
@@ -236,6 +312,45 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.entry = op->entry.p;
     a.pre_scale = pre;
     a.post_scale = post;
+    // few planes: the x sweep's lanes would be planes, mostly idle; run it as
+    // a y sweep (lanes = rows) on the transposed field instead. Opt-in
+    // (RGF_B200_XT=1, read per sweep): 1024^2 single level 2x faster, C3
+    // level 0 slower (one plane leaves 7 of the y CTA's 8 plane-warps idle),
+    // DESIGN §10.
+    const char* xte = std::getenv("RGF_B200_XT");
+    const bool xt_env = xte && xte[0] == '1';
+    if (xt_env && dir == 0 && op->ckpt_ok && !op->ring_ok && nvar * nlev <= 8 && !pre && !post &&
+        rgfb::tma_supported(in, out, pitch)) {
+      if (!op->xt_ok) build_xt(op, st);
+      // transposed rows (length ny) padded to a 16 B pitch for the TMA maps
+      const int64_t q = 16 / static_cast<int64_t>(sizeof(T));
+      const int64_t pt = (op->ny + q - 1) / q * q, planes = nvar * nlev;
+      op->xt_in.alloc(static_cast<size_t>(planes * op->nx * pt) * sizeof(T));
+      op->xt_out.alloc(static_cast<size_t>(planes * op->nx * pt) * sizeof(T));
+      T* ti = reinterpret_cast<T*>(op->xt_in.p);
+      T* to = reinterpret_cast<T*>(op->xt_out.p);
+      transpose_planes<T>(in, ti, op->nx, op->ny, pitch, pt, planes, st);
+      rgfb::StreamArgs b = a;
+      b.dir = 1;
+      b.nx = op->ny;
+      b.ny = op->nx;
+      b.pitch = pt;
+      b.c3 = op->xt_c3.p;
+      b.c3s = op->xt_c3s.p;
+      b.idc = op->unit_dc ? op->xt_idc.p : nullptr;
+      b.idcp = b.idc;
+      b.ipitch = (op->ny + 1) / 2 * 2;
+      b.bitsT = op->xt_bitsT.p;
+      b.words = op->words[0];
+      b.clos = op->xt_clos.p;
+      op->ckpt.alloc(static_cast<size_t>(std::max<int64_t>(1, rgfb::ckpt_doubles<T>(b))));
+      op->launches +=
+          static_cast<unsigned long long>(rgfb::launch_ckpt_sweep<T>(ti, to, b, op->ckpt.p, st));
+      CUDA_OK(cudaGetLastError());
+      transpose_planes<T>(to, out, op->ny, op->nx, pt, pitch, planes, st);
+      op->launches += 2;
+      return;
+    }
     if (op->ckpt_ok && op->ring_ok && rgfb::tma_supported(in, out, pitch)) {
       op->launches += static_cast<unsigned long long>(rgfb::launch_ring_sweep<T>(in, out, a, st));
       CUDA_OK(cudaGetLastError());
@@ -828,6 +943,7 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
           cls[l] = static_cast<int>(it - classes.begin());
         }
         op->nclass = static_cast<int>(classes.size());
+        op->class_g = classes;
         op->cls_d.upload(cls.data(), cls.size());
         op->clos.alloc(static_cast<size_t>(op->nclass) * 2 * 2 * nh * 10);
         const int threads = 128;

@@ -549,3 +549,30 @@ def test_rf1_block_multiple_rows(P, nx, dt):
         want = cpu.apply(getattr(O, name), f.astype(np.float64))
         assert relmax(got, want) <= tol, (name, relmax(got, want))
         assert np.all(got[:, ~g["mask"]] == 0.0), name
+
+
+@pytest.mark.parametrize("nlev,nvar,nx,ny,dt", [(1, 1, 96, 64, "f64"), (3, 2, 128, 40, "f64"),
+                                                (1, 1, 160, 48, "f32"), (2, 1, 57, 44, "f64"),
+                                                (1, 1, 64, 43, "f64"), (1, 1, 96, 45, "f32")])
+def test_few_plane_x_sweep_transposed(P, monkeypatch, nlev, nvar, nx, ny, dt):
+    """RGF_B200_XT=1: with <= 8 planes the x sweep runs as a y sweep on the transposed field
+    (lanes = rows; x tables built in the transposed frame, closures
+    included; odd ny pads the transposed rows to a 16 B pitch): every kind
+    against the oracle, in place too, with variance and per-level masks."""
+    monkeypatch.setenv("RGF_B200_XT", "1")  # opt-in, read per sweep
+    g, rx, ry = random_case(990 + nx + nlev, nx=nx, ny=ny, nlev=nlev, sea=0.7)
+    var = np.random.default_rng(27).uniform(0.5, 2.0, (nlev, ny, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
+    f = np.random.default_rng(28).standard_normal((nvar, nlev, ny, nx))
+    tol = TOL64
+    if dt == "f32":
+        f = f.astype(np.float32)
+        tol = TOL32
+    for name in KINDS:
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f.astype(np.float64))
+        assert relmax(got, want) <= tol, (name, relmax(got, want))
+        assert np.all(got[:, ~g["mask"]] == 0.0), name
+    h = f.copy()
+    gpu.apply(P.GX, h, out=h)
+    assert relmax(h, cpu.apply(O.GX, f.astype(np.float64))) <= tol
