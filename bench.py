@@ -383,7 +383,9 @@ def main():
                                                      f"{dom}-sweep"),
                          "kernel": f"{dom}-sweep", "peak_source": peak_src,
                          "bytes_per_launch": bytes_sweep,
-                         "xy_bytes_alg_GBs": xy_gbs, "xy_frac": xy_gbs / peak},
+                         "xy_bytes_alg_GBs": xy_gbs, "xy_frac": xy_gbs / peak,
+                         # BASELINE.json north_star quotes B200's ~8 TB/s nominal
+                         "xy_frac_vs_nominal_8000": xy_gbs / 8000.0},
             "sweep_ms": sweep_ms,
             "e2e": e2e,
             "gpu_launches": launches,
