@@ -3,10 +3,13 @@
 diagnostics.cpp:182's timed unit) on synthetic BASELINE.json grids.
 
 Default workload: config C5 (4320x2160x100 levels, fp64, 3rd-RF, reference
-default options: unit_dc, YvV95, ghost width ceil(9 max sigma)). Levels are
-sharded across ranks (one process per GPU, torchrun), no collective on the
-data path; weak scaling (every rank owns 100 levels of the same horizontal
-grid). Prints ONE JSON line on rank 0.
+default options: unit_dc, YvV95, ghost width ceil(9 max sigma)). Under
+torchrun (N>1) the 100 levels are sharded across ranks (strong scaling,
+SURVEY §8e / BASELINE configs[4]): each rank filters its contiguous level
+block with no collective on the data path; the result is gathered to rank 0
+afterwards with grouped NCCL point-to-point (reported as `gather`, not in
+`value`). `--scaling weak` gives every rank the full level set instead.
+Prints ONE JSON line on rank 0.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl reference]
 """
@@ -49,6 +52,11 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N>1: shard the config's levels (strong) or replicate them (weak)")
+    ap.add_argument("--ref-budget-s", type=float, default=420.0,
+                    help="reference arm: whole-run CPU budget; above it each step times a "
+                         "level sample instead of the full level set")
     ap.add_argument("--no-extra", action="store_true",
                     help="skip the 1st-RF / fp32 / adjoint figures (reported by default on 1 GPU)")
     return ap.parse_args()
@@ -133,72 +141,119 @@ def dist_init():
     return world, rank, local
 
 
-class CpuPort:
-    """The oracle (C++ restatement of the reference, all host threads) on a
-    bounded level sample of the same workload: the operator and the sample
-    field are built once; each run() times one x+y application."""
+def load_synth():
+    """paper_1404_5756_b200/synth.py as a standalone module: the input
+    generators without the package (whose import maps librgf_b200.so), so the
+    reference arm's process never loads the product library."""
+    import importlib.util
+    path = os.path.join(ROOT, "paper_1404_5756_b200", "synth.py")
+    spec = importlib.util.spec_from_file_location("rgf_bench_synth", path)
+    mod = importlib.util.module_from_spec(spec)
+    sys.modules[spec.name] = mod
+    spec.loader.exec_module(mod)
+    return mod
 
-    def __init__(self, cfg, order, k, seconds, levels_cap=None):
+
+def workload_config(args, cfg, k):
+    """The `config` object, identical for both arms and every N."""
+    return {"workload": f"{args.config} ({cfg.description}) x+y apply_gy.apply_gx, "
+                        f"order={args.order} k={k}",
+            "nx": cfg.nx, "ny": cfg.ny, "nlev": cfg.nlev, "nvar": cfg.nvar,
+            "l2": "inputs larger than L2 (field >> 126 MB)",
+            "options": "unit_dc=1 yvv95 ghost=ceil(9 max sigma) per level"}
+
+
+class CpuPort:
+    """The oracle (C++ restatement of the reference) on `threads` host
+    threads over levels [0, nl) of the same workload: the operator and the
+    input field are built once; each run() times one x+y application."""
+
+    def __init__(self, cfg, order, k, threads, nl):
         import oracle as O
         self.O = O
-        self.cfg = cfg
-        self.threads = os.cpu_count() or 1
+        self.threads = threads
         self.op = O.OracleOp(cfg.nx, cfg.ny, cfg.dx, cfg.dy, cfg.mask, cfg.rx, cfg.ry,
-                             order=order, k_iterations=k, threads=self.threads)
-        rng = np.random.default_rng(99)
-        f1 = rng.standard_normal((1, 1, cfg.ny, cfg.nx))
-        t0 = time.perf_counter()
-        self.op.apply(O.GYGX, f1, lev0=0, nlev_sub=1)
-        t1 = time.perf_counter() - t0
-        nl = max(1, min(cfg.nlev, int(seconds / max(t1, 1e-6))))
-        if levels_cap:
-            nl = min(nl, levels_cap)
-        self.nl = nl
-        self.f = rng.standard_normal((1, nl, cfg.ny, cfg.nx))
-        pts = cfg.nx * cfg.ny * nl
-        self.pts = pts
-        self.sample = f"{nl} of {cfg.nlev} levels ({pts} points), 1 application"
+                             order=order, k_iterations=k, threads=threads)
+        self.nl = max(1, min(cfg.nlev, nl))
+        self.f = np.random.default_rng(99).standard_normal((cfg.nvar, self.nl, cfg.ny, cfg.nx))
+        self.pts = cfg.nx * cfg.ny * self.nl * cfg.nvar
+        self.sample = (f"{self.nl} of {cfg.nlev} levels x {cfg.nvar} var ({self.pts} points), "
+                       f"1 x+y application")
 
     def run(self):
+        """(Gpt/s, seconds) of one timed application."""
         t0 = time.perf_counter()
         self.op.apply(self.O.GYGX, self.f, lev0=0, nlev_sub=self.nl)
-        return self.pts / (time.perf_counter() - t0) / 1e9
+        dt = time.perf_counter() - t0
+        return self.pts / dt / 1e9, dt
 
 
-def cpu_port_rate(cfg, order, k, seconds, levels_cap=None):
-    """One timed oracle application on a level sample; (Gpt/s, sample, cores)."""
-    cp = CpuPort(cfg, order, k, seconds, levels_cap)
-    return cp.run(), cp.sample, cp.threads
+def levels_for(cfg, order, k, threads, seconds):
+    """Levels of `cfg` one application covers in about `seconds`."""
+    probe = CpuPort(cfg, order, k, threads, 1)
+    probe.run()
+    _, t1 = probe.run()
+    return max(1, min(cfg.nlev, int(seconds / max(t1, 1e-6)))), t1
+
+
+def cpu_baselines(cfg, order, k, seconds):
+    """cpu_baseline (all host threads, ~`seconds` of work) and the
+    single-thread figure BASELINE.md §3 asks for (test_output.txt:16)."""
+    cores = os.cpu_count() or 1
+    nl, _ = levels_for(cfg, order, k, cores, seconds)
+    cp = CpuPort(cfg, order, k, cores, nl)
+    v, _ = cp.run()
+    one = CpuPort(cfg, order, k, 1, 1)
+    v1, _ = one.run()
+    return ({"value": v, "unit": "Gpoints/s", "cores": cores, "kind": "port",
+             "sample": cp.sample},
+            {"value": v1, "unit": "Gpoints/s", "cores": 1, "kind": "port",
+             "sample": one.sample})
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU algorithm (oracle port; the
-    reference itself is unbuildable here) with every host thread."""
+    """--impl reference: the reference's CPU algorithm on every host thread.
+    The reference cannot be built here (Eigen3/CLI11/doctest absent), so this
+    is the oracle port (oracle/, a line-by-line restatement pinned to the
+    reference's golden vectors). Each step is one timed x+y application over
+    the whole config (all levels) unless (warmup+steps) of those would exceed
+    --ref-budget-s; then each step covers a level sample and the line says so.
+    ms_per_step is the measured time of one step either way."""
     if rank != 0:
         return
-    from paper_1404_5756_b200 import synth
+    synth = load_synth()
     cfg = synth.make_config(args.config, nlev=args.nlev)
     k = args.k or (5 if args.order == 1 else 1)
-    # operator and level sample built once; each step is one timed x+y
-    # application of ~2 s of CPU work (the whole default run stays ~1 min)
-    cp = CpuPort(cfg, args.order, k, 2.0)
-    rates = []
-    for i in range(args.warmup + args.steps):
-        r = cp.run()
+    cores = os.cpu_count() or 1
+    _, t1 = levels_for(cfg, args.order, k, cores, 1.0)
+    runs = args.warmup + args.steps
+    nl = cfg.nlev
+    if runs * t1 * cfg.nlev > args.ref_budget_s:
+        nl = max(1, int(args.ref_budget_s / (runs * t1)))
+    cp = CpuPort(cfg, args.order, k, cores, nl)
+    rates, secs = [], []
+    for i in range(runs):
+        r, dt = cp.run()
         if i >= args.warmup:
             rates.append(r)
-    v = statistics.median(rates)
-    sample, cores = cp.sample, cp.threads
-    line = {"impl": "reference", "metric": metric_name(args.order, args.k or (5 if args.order == 1 else 1)),
+            secs.append(dt)
+    v = cp.pts * len(secs) / sum(secs) / 1e9
+    one = CpuPort(cfg, args.order, k, 1, 1)
+    v1, _ = one.run()
+    line = {"impl": "reference", "metric": metric_name(args.order, k),
             "value": v, "unit": "Gpoints/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": cfg.nx * cfg.ny * cfg.nlev * cfg.nvar / (v * 1e9) * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-            "dtype": "f64", "data": "synthetic",
-            "config": {"workload": f"{args.config} ({cfg.description}) order={args.order} k={k}",
-                       "nx": cfg.nx, "ny": cfg.ny, "nlev": cfg.nlev, "nvar": cfg.nvar},
+            "ms_per_step": statistics.mean(secs) * 1e3,
+            "higher_is_better": True, "scaling": "strong" if args.scaling == "strong" else "weak",
+            "vs_baseline": None, "dtype": args.dtype, "data": "synthetic",
+            "config": workload_config(args, cfg, k),
             "cpu_baseline": {"value": v, "unit": "Gpoints/s", "cores": cores, "kind": "port",
-                             "sample": sample + " per step"},
+                             "sample": cp.sample + " per step" +
+                             ("" if nl == cfg.nlev else " (level sample: full set over budget)")},
+            "cpu_baseline_1thread": {"value": v1, "unit": "Gpoints/s", "cores": 1,
+                                     "kind": "port", "sample": one.sample},
+            "note": "the oracle computes in fp64 whatever --dtype says (the reference has no "
+                    "fp32 operator, types.hpp:14)",
             "e2e": {"value": v, "unit": "Gpoints/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -218,31 +273,40 @@ def main():
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     import paper_1404_5756_b200 as P
     from paper_1404_5756_b200 import synth
+    from paper_1404_5756_b200.sharding import (ShardedCovarianceOp, gather_levels,
+                                               level_range)
 
     cfg = synth.make_config(args.config, nlev=args.nlev)
     k = args.k or (5 if args.order == 1 else 1)
     tdt = torch.float64 if args.dtype == "f64" else torch.float32
     w = 8 if args.dtype == "f64" else 4
-    grid = P.Grid2D(cfg.nx, cfg.ny, cfg.dx, cfg.dy, cfg.mask)
+    strong = args.scaling == "strong"
+    # this rank's level block: a contiguous shard (strong) or all levels (weak)
+    sw, sr = (world, rank) if strong else (1, 0)
     opts = P.CovarianceOptions(order=P.FilterOrder(args.order), k_iterations=k, device=local)
     t0 = time.perf_counter()
-    op = P.HorizontalCovarianceOp(grid, P.ScaleField(cfg.rx, cfg.ry), opts)
+    sop = ShardedCovarianceOp(cfg.nx, cfg.ny, cfg.dx, cfg.dy, cfg.mask, cfg.rx, cfg.ry, opts,
+                              nlev=cfg.nlev, world=sw, rank=sr)
     build_s = time.perf_counter() - t0
-    shape = (cfg.nvar, cfg.nlev, cfg.ny, cfg.nx)
+    nl_local = sop.nlev_local
+    shape = (cfg.nvar, nl_local, cfg.ny, cfg.nx)
     gen = torch.Generator(device="cuda").manual_seed(1000 + rank)
     x = torch.randn(shape, generator=gen, device="cuda", dtype=torch.float64).to(tdt)
     y = torch.empty_like(x)
     stream = torch.cuda.current_stream()
 
     def step():
-        op.apply(P.GYGX, x, y)
+        sop.apply(P.GYGX, x, y)
+
+    def launches_now():
+        return sop.op.launch_count() if sop.op is not None else 0
 
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    l0 = op.launch_count()
+    l0 = launches_now()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
@@ -255,80 +319,96 @@ def main():
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
-    launches = op.launch_count() - l0
+    launches = launches_now() - l0
     ms = e0.elapsed_time(e1) / args.steps
     if world > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
-    n_rank = cfg.nx * cfg.ny * cfg.nlev * cfg.nvar
-    value = n_rank * world / (ms * 1e-3) / 1e9
+        lt = torch.tensor([launches], device="cuda", dtype=torch.float64)
+        dist.all_reduce(lt)
+        launches = int(lt.item())
+    n_local = cfg.nx * cfg.ny * nl_local * cfg.nvar
+    n_total = cfg.nx * cfg.ny * cfg.nlev * cfg.nvar * (1 if strong else world)
+    value = n_total / (ms * 1e-3) / 1e9
 
     # final gather of the result into rank 0's field over NCCL (outside the
-    # timed region; levels need no other exchange)
+    # timed region; levels need no other exchange), device-timed, max over ranks
     gather = None
     if world > 1:
-        from paper_1404_5756_b200.sharding import gather_levels
+        nlev_all = cfg.nlev * (1 if strong else world)
         torch.cuda.synchronize()
         dist.barrier()
-        g0 = time.perf_counter()
-        full = gather_levels(y, cfg.nlev * world)
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        full = gather_levels(y, nlev_all)
+        g1.record(stream)
         torch.cuda.synchronize()
-        gather = {"ms": (time.perf_counter() - g0) * 1e3, "bytes": n_rank * w * world,
-                  "timing": "host wall clock, NCCL gather to rank 0 (not in value)"}
+        t = torch.tensor([g0.elapsed_time(g1)], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        gms = float(t.item())
+        gather = {"ms": gms, "bytes_into_rank0": (n_total - n_local) * w,
+                  "compute_plus_gather_ms": ms + gms,
+                  "timing": "CUDA events around grouped NCCL send/recv to rank 0, max over "
+                            "ranks (not in value)"}
         del full
 
     # per-kernel timing of the two directional sweeps (dominant kernel)
     sweep_ms = {}
-    for name, kind in (("x", P.GX), ("y", P.GY)):
-        for _ in range(2):
-            op.apply(kind, x, y)
-        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        a.record(stream)
-        reps = max(3, args.steps // 2)
-        for _ in range(reps):
-            op.apply(kind, x, y)
-        b.record(stream)
-        torch.cuda.synchronize()
-        sweep_ms[name] = a.elapsed_time(b) / reps
-    dom = max(sweep_ms, key=sweep_ms.get)
+    if sop.op is not None:
+        for name, kind in (("x", P.GX), ("y", P.GY)):
+            for _ in range(2):
+                sop.apply(kind, x, y)
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            reps = max(3, args.steps // 2)
+            for _ in range(reps):
+                sop.apply(kind, x, y)
+            b.record(stream)
+            torch.cuda.synchronize()
+            sweep_ms[name] = a.elapsed_time(b) / reps
+    dom = max(sweep_ms, key=sweep_ms.get) if sweep_ms else "y"
     peak, peak_src = peaks()
     nh = cfg.nx * cfg.ny
     coef_words = 4 if args.order == 3 else 2  # per direction (coefficient_bytes()/2)
-    bytes_sweep = n_rank * 2 * w + nh * coef_words * 8
-    achieved = bytes_sweep / (sweep_ms[dom] * 1e-3) / 1e9
-    bytes_xy = synth.bytes_alg(cfg, args.order, w)
-    xy_gbs = bytes_xy / (ms * 1e-3) / 1e9
+    bytes_sweep = n_local * 2 * w + nh * coef_words * 8
+    achieved = bytes_sweep / (sweep_ms[dom] * 1e-3) / 1e9 if sweep_ms else 0.0
+    bytes_xy = synth.bytes_alg(cfg, args.order, w) * (1 if strong else world)
+    xy_gbs = bytes_xy / (ms * 1e-3) / 1e9 / world  # per GPU
 
-    # e2e through the public API with pinned host buffers
+    # e2e through the public API with pinned host buffers: every rank moves
+    # its own levels host->device->host (direct per-GPU D2H)
     e2e = None
     if args.e2e_steps > 0:
         hx = torch.empty(shape, dtype=tdt, pin_memory=True)
         hx.copy_(x)
         hy = torch.empty(shape, dtype=tdt, pin_memory=True)
         hxn, hyn = hx.numpy(), hy.numpy()
-        op.apply(P.GYGX, hxn)  # warm the host-path buffers
+        if sop.op is not None:
+            sop.apply(P.GYGX, hxn, out=hyn)  # warm the host-path buffers
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
         for _ in range(args.e2e_steps):
-            res = op.apply(P.GYGX, hxn, out=hyn)
+            if sop.op is not None:
+                sop.apply(P.GYGX, hxn, out=hyn)
         e2e_s = (time.perf_counter() - t0) / args.e2e_steps
         if world > 1:
             t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             e2e_s = float(t.item())
-        del res
-        e2e = {"value": n_rank * world / e2e_s / 1e9, "unit": "Gpoints/s",
-               "h2d_bytes_per_step": n_rank * w * world, "d2h_bytes_per_step": n_rank * w * world,
+        e2e = {"value": n_total / e2e_s / 1e9, "unit": "Gpoints/s",
+               "h2d_bytes_per_step": n_total * w, "d2h_bytes_per_step": n_total * w,
                "steps": args.e2e_steps, "timing": "host wall clock around the synchronous "
-               "rgf_op_apply(RGF_HOST) call (pinned buffers; H2D + kernels + D2H)"}
+               "rgf_op_apply(RGF_HOST) call (pinned buffers; H2D + kernels + D2H), max over ranks"}
 
     # Other figures BASELINE.json's metric names (1st-RF, fp32, the adjoint):
     # same config and timing method (device-resident, CUDA events, warm-up),
     # reported beside the headline, not in `value`.
     extra = {}
     if world == 1 and args.order == 3 and args.dtype == "f64" and not args.no_extra:
+        grid = P.Grid2D(cfg.nx, cfg.ny, cfg.dx, cfg.dy, cfg.mask)
+
         def timed(op2, kind, x2, y2, reps=3):
             for _ in range(2):
                 op2.apply(kind, x2, y2)
@@ -343,10 +423,10 @@ def main():
 
         def entry(m2, order2, w2):
             ba = synth.bytes_alg(cfg, order2, w2)
-            return {"ms": m2, "Gpt/s": n_rank / (m2 * 1e-3) / 1e9,
+            return {"ms": m2, "Gpt/s": n_local / (m2 * 1e-3) / 1e9,
                     "xy_frac": ba / (m2 * 1e-3) / 1e9 / peaks()[0]}
 
-        m_adj = timed(op, P.VT, x, y)
+        m_adj = timed(sop.op, P.VT, x, y)
         extra["3rd-RF adjoint VT f64"] = entry(m_adj, 3, 8)
         for label, o2, k2, dt2, w2 in (("1st-RF K=5 f64", 1, 5, torch.float64, 8),
                                        ("3rd-RF f32", 3, 1, torch.float32, 4)):
@@ -359,31 +439,29 @@ def main():
             del op2, x2, y2
         extra["t(1st-RF K=5)/t(3rd-RF)"] = extra["1st-RF K=5 f64"]["ms"] / ms
 
-    cpu = None
+    cpu = cpu1 = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, sample, cores = cpu_port_rate(cfg, args.order, k, args.cpu_seconds)
-        cpu = {"value": v, "unit": "Gpoints/s", "cores": cores, "kind": "port",
-               "sample": sample}
+        cpu, cpu1 = cpu_baselines(cfg, args.order, k, args.cpu_seconds)
 
     if rank == 0:
         line = {
             "metric": metric_name(args.order, k), "value": value, "unit": "Gpoints/s",
             "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "higher_is_better": True, "scaling": "strong" if strong else "weak",
+            "vs_baseline": None,
             "dtype": args.dtype, "data": "synthetic",
-            "config": {"workload": f"{args.config} ({cfg.description}) x+y apply_gy.apply_gx, "
-                       f"order={args.order} k={k}, levels sharded ({cfg.nlev} per rank)",
-                       "nx": cfg.nx, "ny": cfg.ny, "nlev_per_rank": cfg.nlev, "nvar": cfg.nvar,
-                       "l2": "inputs larger than L2 (field >> 126 MB)",
-                       "options": "unit_dc=1 yvv95 ghost=ceil(9 max sigma) per level"},
+            "config": workload_config(args, cfg, k),
+            "sharding": {"mode": args.scaling, "levels_per_rank": [
+                level_range(cfg.nlev, sw, r)[1] for r in range(sw)] if strong else cfg.nlev,
+                "collective_on_data_path": False},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak,
                          "traffic": measured_traffic(args.config, args.dtype, args.order,
                                                      f"{dom}-sweep"),
                          "kernel": f"{dom}-sweep", "peak_source": peak_src,
                          "bytes_per_launch": bytes_sweep,
-                         "xy_bytes_alg_GBs": xy_gbs, "xy_frac": xy_gbs / peak,
+                         "xy_bytes_alg_GBs_per_gpu": xy_gbs, "xy_frac": xy_gbs / peak,
                          # BASELINE.json north_star quotes B200's ~8 TB/s nominal
                          "xy_frac_vs_nominal_8000": xy_gbs / 8000.0},
             "sweep_ms": sweep_ms,
@@ -391,6 +469,7 @@ def main():
             "gpu_launches": launches,
             "clocks": clk.summary(),
             "cpu_baseline": cpu,
+            "cpu_baseline_1thread": cpu1,
             "build_seconds": build_s,
         }
         if gather:

@@ -305,7 +305,14 @@ class HorizontalCovarianceOp:
             raise InvalidArgument("apply: field is not on the expected grid")
         f = np.ascontiguousarray(f)
         nvar = f.size // (nx * ny * nlev)
-        res = np.empty_like(f) if out is None else out
+        if out is None:
+            res = np.empty_like(f)
+        else:  # the C ABI writes f.nbytes through this pointer: check it first
+            res = out
+            if (not isinstance(res, np.ndarray) or res.dtype != f.dtype or res.shape != f.shape
+                    or not res.flags.c_contiguous or not res.flags.writeable):
+                raise InvalidArgument("apply: out must be a writeable C-contiguous array with "
+                                      "the field's dtype and shape")
         dtype = F64 if f.dtype == np.float64 else F32
         _check(lib.rgf_op_apply(self._h, kind, dtype, _ptr(f), _ptr(res), nvar, HOST, None))
         return res
@@ -319,8 +326,18 @@ class HorizontalCovarianceOp:
             raise InvalidArgument("apply: expected a contiguous float64/float32 tensor")
         if tuple(field.shape[-2:]) != (ny, nx) or field.numel() % (nx * ny * nlev):
             raise InvalidArgument("apply: field is not on the expected grid")
+        if field.device != torch.device("cuda", int(self.options_.device)):
+            raise InvalidArgument("apply: field is not on the operator's device")
         nvar = field.numel() // (nx * ny * nlev)
-        res = torch.empty_like(field) if out is None else out
+        if out is None:
+            res = torch.empty_like(field)
+        else:
+            res = out
+            if (not isinstance(res, torch.Tensor) or res.dtype != field.dtype
+                    or res.shape != field.shape or res.device != field.device
+                    or not res.is_contiguous()):
+                raise InvalidArgument("apply: out must be a contiguous tensor with the field's "
+                                      "dtype, shape and device")
         dtype = F64 if field.dtype == torch.float64 else F32
         st = stream if stream is not None else torch.cuda.current_stream(field.device)
         _check(lib.rgf_op_apply(self._h, kind, dtype, field.data_ptr(), res.data_ptr(), nvar,

@@ -24,9 +24,7 @@
 #include "sweep_stream.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_ckpt.cuh"
-#include "sweep_ring.cuh"
 #include "rf1_stream.cuh"
-#include "rf1_seg.cuh"
 #include "closures.cuh"
 #include "solver_kernels.cuh"
 
@@ -111,8 +109,6 @@ struct DirData {
   std::vector<int64_t> seg_off_h;  // host copy (1st-RF level-chunk segment ranges)
   DevBuf<int2> segs;
   DevBuf<int32_t> seg_line;  // per segment: lev*lines + line
-  DevBuf<int32_t> lpt_ord;   // 1st-RF line-resident kernel: each line's segments, longest first
-  int lpt_B = 0;             // lpt_ord built
   DevBuf<int64_t> close_order;  // segments sorted by (line, end, level)
   int64_t nsegs = 0;
   std::vector<char> uniform;        // per level
@@ -140,8 +136,8 @@ struct rgf_op {
   unsigned long long launches = 0;
   // streaming 3rd-RF path: bit-packed masks, closure classes and tables
   bool stream_ok = false;
-  bool ckpt_ok = true;  // checkpointed 3-pass sweeps (RGF_B200_TWOPASS=1: two-pass kernels)
-  bool ring_ok = false;  // single-pass ring sweeps (experimental: RGF_B200_SWEEP=ring)
+  bool ckpt_ok = true;  // TMA-fed sweeps (checkpointed / single-pass) for this op's tables
+  bool xt_env = false;   // RGF_B200_XT=1 at creation: few-plane x sweeps on the transposed field
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
@@ -175,6 +171,13 @@ struct rgf_op {
     CUDA_OK(cudaEventCreateWithFlags(&pipe_ev_user, cudaEventDisableTiming));
   }
   std::mutex mu;  // apply() is const in the reference; serialize buffer reuse
+  // Apply scratch (tmp1/tmp2, ckpt, entry, rf1 histories, pitched and pipeline
+  // slots) is shared by every apply of this op. The host lock only orders the
+  // enqueueing, so each apply's first stream waits on this event and its last
+  // stream records it: two applies on different streams (or a device apply
+  // followed by a host one) never overlap on the scratch.
+  cudaEvent_t scratch_free = nullptr;
+  int64_t chunk_mb = 256;  // host-apply pipeline chunk (RGF_B200_CHUNK_MB at creation)
 
   ~rgf_op() {
     if (own_stream) cudaStreamDestroy(own_stream);
@@ -184,6 +187,7 @@ struct rgf_op {
       for (auto e : row)
         if (e) cudaEventDestroy(e);
     if (pipe_ev_user) cudaEventDestroy(pipe_ev_user);
+    if (scratch_free) cudaEventDestroy(scratch_free);
   }
 };
 
@@ -317,9 +321,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     // (RGF_B200_XT=1, read per sweep): 1024^2 single level 2x faster, C3
     // level 0 slower (one plane leaves 7 of the y CTA's 8 plane-warps idle),
     // DESIGN §10.
-    const char* xte = std::getenv("RGF_B200_XT");
-    const bool xt_env = xte && xte[0] == '1';
-    if (xt_env && dir == 0 && op->ckpt_ok && !op->ring_ok && nvar * nlev <= 8 && !pre && !post &&
+    if (op->xt_env && dir == 0 && op->ckpt_ok && nvar * nlev <= 8 && !pre && !post &&
         rgfb::tma_supported(in, out, pitch)) {
       if (!op->xt_ok) build_xt(op, st);
       // transposed rows (length ny) padded to a 16 B pitch for the TMA maps
@@ -349,11 +351,6 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
       CUDA_OK(cudaGetLastError());
       transpose_planes<T>(to, out, op->ny, op->nx, pt, pitch, planes, st);
       op->launches += 2;
-      return;
-    }
-    if (op->ckpt_ok && op->ring_ok && rgfb::tma_supported(in, out, pitch)) {
-      op->launches += static_cast<unsigned long long>(rgfb::launch_ring_sweep<T>(in, out, a, st));
-      CUDA_OK(cudaGetLastError());
       return;
     }
     if (op->ckpt_ok && rgfb::tma_supported(in, out, pitch)) {
@@ -398,28 +395,6 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.ent = op->rf1_ent.p;
     a.pre_scale = pre;
     a.post_scale = post;
-    // line-resident kernel (all K iterations in one pass, experimental:
-    // RGF_B200_RF1=line) when the line group fits in shared memory; the
-    // 2K-pass streaming kernels are the default (faster)
-    const char* rv = std::getenv("RGF_B200_RF1");
-    const bool seg = rv && std::strcmp(rv, "line") == 0;
-    if (seg) {  // per-line segment order (longest first), built on first use
-      DirData& dm = dir == 0 ? op->dx_ : op->dy_;
-      const int64_t nl = op->nlev * (dir == 0 ? op->ny : op->nx);
-      if (!dm.lpt_B && dm.nsegs > 0) {
-        dm.lpt_ord.alloc(static_cast<size_t>(dm.nsegs));
-        rgfb::k_rf1_sort<<<grid_for(nl, 128, 148 * 16), 128, 0, st>>>(dm.seg_off.p, dm.segs.p, nl,
-                                                                    dm.lpt_ord.p);
-        CUDA_OK(cudaGetLastError());
-        dm.lpt_B = 1;
-      }
-      if (dm.lpt_B) a.lpt_ord = dm.lpt_ord.p;
-    }
-    if (seg && a.lpt_ord != nullptr && rgfb::launch_rf1_seg<T>(in, out, a, st)) {
-      op->launches += 1;
-      CUDA_OK(cudaGetLastError());
-      return;
-    }
     op->launches += static_cast<unsigned long long>(rgfb::launch_rf1_sweep<T>(in, out, a, st));
     CUDA_OK(cudaGetLastError());
     return;
@@ -521,8 +496,7 @@ void apply_host_pipelined(rgf_op* op, int kind, const T* hin, T* hout, int64_t n
   const int64_t nlev = op->nlev;
   // ~256 MB per chunk, >= 1 level; at least 4 chunks per variable when possible
   const int64_t per_level = nh * static_cast<int64_t>(sizeof(T));
-  int64_t chunk_mb = 256;
-  if (const char* e = std::getenv("RGF_B200_CHUNK_MB")) chunk_mb = std::max(1L, std::atol(e));
+  const int64_t chunk_mb = op->chunk_mb;
   int64_t cl = std::max<int64_t>(1, (chunk_mb << 20) / per_level);
   cl = std::min(cl, std::max<int64_t>(1, (nlev + 3) / 4));
   // The x kernels give each lane a plane and walk a whole row per CTA, so a
@@ -546,6 +520,9 @@ void apply_host_pipelined(rgf_op* op, int kind, const T* hin, T* hout, int64_t n
   CUDA_OK(cudaEventRecord(op->pipe_ev_user, user));
   CUDA_OK(cudaStreamWaitEvent(h2d, op->pipe_ev_user, 0));
   CUDA_OK(cudaStreamWaitEvent(cs, op->pipe_ev_user, 0));
+  // and after every earlier apply of this op (shared scratch), on any stream
+  CUDA_OK(cudaStreamWaitEvent(h2d, op->scratch_free, 0));
+  CUDA_OK(cudaStreamWaitEvent(cs, op->scratch_free, 0));
   int64_t c = 0;
   for (int64_t v = 0; v < nvar; ++v)
     for (int64_t l0 = 0; l0 < nlev; l0 += cl, ++c) {
@@ -571,6 +548,7 @@ void apply_host_pipelined(rgf_op* op, int kind, const T* hin, T* hout, int64_t n
                                 cudaMemcpyDeviceToHost, d2h));
       CUDA_OK(cudaEventRecord(ev[2], d2h));
     }
+  CUDA_OK(cudaEventRecord(op->scratch_free, d2h));  // d2h waited on every compute chunk
   CUDA_OK(cudaStreamSynchronize(d2h));
 }
 
@@ -971,10 +949,8 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
         CUDA_OK(cudaDeviceSynchronize());
         op->stream_ok = true;
-        const char* tp = std::getenv("RGF_B200_TWOPASS");
-        op->ckpt_ok = !(tp && tp[0] == '1');
-        const char* sv = std::getenv("RGF_B200_SWEEP");
-        op->ring_ok = sv && std::strcmp(sv, "ring") == 0;
+        const char* xte = std::getenv("RGF_B200_XT");
+        op->xt_env = xte && xte[0] == '1';
         if (op->ckpt_ok) {
           for (int dir = 0; dir < 2; ++dir) {
             const int64_t tot = g->nlev * (dir == 0 ? g->ny : g->nx) * op->words[dir];
@@ -1040,6 +1016,9 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
       op->has_variance = true;
     }
     CUDA_OK(cudaStreamCreateWithFlags(&op->own_stream, cudaStreamNonBlocking));
+    CUDA_OK(cudaEventCreateWithFlags(&op->scratch_free, cudaEventDisableTiming));
+    if (const char* e = std::getenv("RGF_B200_CHUNK_MB"))
+      op->chunk_mb = std::max<int64_t>(1, std::atol(e));
     CUDA_OK(cudaDeviceSynchronize());
     *out = op.release();
   });
@@ -1075,12 +1054,14 @@ int rgf_op_apply(rgf_op* op, int kind, int dtype, const void* in, void* out, int
       return;
     }
     if (memory != RGF_DEVICE) throw InvalidArgument("apply: unknown memory kind");
+    CUDA_OK(cudaStreamWaitEvent(st, op->scratch_free, 0));
     if (dtype == RGF_F64)
       apply_device<double>(op, kind, static_cast<const double*>(in), static_cast<double*>(out),
                            nvar, st);
     else
       apply_device<float>(op, kind, static_cast<const float*>(in), static_cast<float*>(out), nvar,
                           st);
+    CUDA_OK(cudaEventRecord(op->scratch_free, st));
   });
 }
 
@@ -1373,6 +1354,11 @@ int rgf_cost(rgf_op* op, rgf_obs* o, const double* chi, const double* background
     std::lock_guard<std::mutex> lock(op->mu);
     CUDA_OK(cudaSetDevice(op->device));
     cudaStream_t st = nullptr;
+    CUDA_OK(cudaStreamWaitEvent(st, op->scratch_free, 0));
+    struct Rec {
+      rgf_op* op;
+      ~Rec() { cudaEventRecord(op->scratch_free, nullptr); }
+    } rec{op};
     Cg cg{op, o, st, op->nx * op->ny, {}, {}, {}, {}, {}};
     cg.init();
     const int64_t nh = cg.nh, n = o->n;
@@ -1414,6 +1400,11 @@ int rgf_solve(rgf_op* op, rgf_obs* o, double tol, int32_t max_iter, const double
     std::lock_guard<std::mutex> lock(op->mu);
     CUDA_OK(cudaSetDevice(op->device));
     cudaStream_t st = nullptr;
+    CUDA_OK(cudaStreamWaitEvent(st, op->scratch_free, 0));
+    struct Rec {
+      rgf_op* op;
+      ~Rec() { cudaEventRecord(op->scratch_free, nullptr); }
+    } rec{op};
     Cg cg{op, o, st, op->nx * op->ny, {}, {}, {}, {}, {}};
     cg.init();
     const int64_t nh = cg.nh, n = o->n;

@@ -545,18 +545,12 @@ __global__ void __launch_bounds__(128) k_x_pass_d(T* __restrict__ out, StreamArg
 }
 
 template <typename T>
-inline bool tma_supported(const T* in, const T* out, int64_t nx);
-template <typename T>
-int launch_tma_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st);
-
-template <typename T>
 int launch_stream_sweep(const T* in, T* out, const StreamArgs& a, cudaStream_t st) {
   const int threads = 128;
   const int64_t planes = a.nvar * a.nlev;
   const int64_t nlines = a.dir == 0 ? a.ny : a.nx;
   const int64_t chains = planes * nlines;
   const int64_t eblocks = (chains + threads - 1) / threads;
-  if (tma_supported(in, out, a.nx)) return launch_tma_sweep<T>(in, out, a, st);
   if (a.dir == 1) {
     constexpr int L = 4, U = 4;
     const int64_t total = ((planes + L - 1) / L) * a.nx;

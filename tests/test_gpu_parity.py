@@ -387,22 +387,6 @@ def test_level_sharded_ops_match_full_op(P):
         assert np.array_equal(np.concatenate(parts, axis=1), want), name
 
 
-@pytest.mark.parametrize("nx", [57, 96])
-def test_two_pass_kernels_still_match(P, monkeypatch, nx):
-    """RGF_B200_TWOPASS=1 keeps the two-pass kernels (TMA pass A/D for
-    aligned rows, the register/cp.async kernels for unaligned rows)."""
-    g, rx, ry = random_case(515 + nx, nx=nx, ny=37, nlev=3)
-    var = np.random.default_rng(13).uniform(0.5, 2.0, (3, 37, nx))
-    monkeypatch.setenv("RGF_B200_TWOPASS", "1")
-    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
-    monkeypatch.delenv("RGF_B200_TWOPASS")
-    f = np.random.default_rng(14).standard_normal((2, 3, 37, nx))
-    for name in KINDS:
-        got = gpu.apply(getattr(P, name), f)
-        want = cpu.apply(getattr(O, name), f)
-        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
-
-
 @pytest.mark.parametrize("nx,dt", [(57, "f64"), (61, "f32"), (58, "f32")])
 def test_unaligned_rows_device_path_pitched(P, nx, dt):
     """Rows whose byte length is not a 16 B multiple run the checkpointed
@@ -449,64 +433,6 @@ def test_rf1_streaming_path(P, monkeypatch, k):
         want = cpu.apply(getattr(O, name), f)
         assert relmax(got, want) <= TOL64, (name, relmax(got, want))
         assert relmax(got, exact.apply(getattr(P, name), f)) <= TOL64, name
-
-
-@pytest.mark.parametrize("nx,ny,sea,dt", [(96, 37, 0.8, "f64"), (400, 300, 1.0, "f64"),
-                                          (57, 43, 0.6, "f64"), (128, 70, 0.8, "f32")])
-def test_ring_sweeps_experimental(P, monkeypatch, nx, ny, sea, dt):
-    """RGF_B200_SWEEP=ring selects the single-pass ring kernels (sweep_ring.cuh,
-    experimental). Per-level masks (warp lanes meet different segment ends),
-    all-sea lines longer than the ring (spills through the output buffer), and
-    unaligned rows (pitched copies), for every kind."""
-    g, rx, ry = random_case(611 + nx, nx=nx, ny=ny, nlev=5, sea=sea)
-    var = np.random.default_rng(15).uniform(0.5, 2.0, (5, ny, nx))
-    monkeypatch.setenv("RGF_B200_SWEEP", "ring")
-    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
-    monkeypatch.delenv("RGF_B200_SWEEP")
-    f = np.random.default_rng(16).standard_normal((2, 5, ny, nx))
-    tol = TOL64
-    if dt == "f32":
-        f = f.astype(np.float32)
-        tol = TOL32
-    for name in KINDS:
-        got = gpu.apply(getattr(P, name), f)
-        want = cpu.apply(getattr(O, name), f.astype(np.float64))
-        assert relmax(got, want) <= tol, (name, relmax(got, want))
-        assert np.all(got[:, ~g["mask"]] == 0.0), name
-
-
-@pytest.mark.parametrize("k,nx,ny,sea,dt", [(1, 70, 44, 0.65, "f64"), (3, 64, 40, 0.8, "f64"),
-                                             (5, 96, 57, 0.6, "f64"), (5, 64, 300, 1.0, "f64"),
-                                             (5, 64, 37, 0.7, "f32"), (8, 32, 20, 0.7, "f64")])
-def test_rf1_line_resident_matches_streaming(P, monkeypatch, k, nx, ny, sea, dt):
-    """The line-resident 1st-RF (rf1_seg.cuh, experimental RGF_B200_RF1=line:
-    a line group in shared memory, lanes = segments, all K iterations, one
-    launch per sweep) is bit-identical to the 2K-pass streaming kernels (the
-    default) and matches the oracle, for every kind, with variance, per-level
-    masks, 300-row columns (several 256-row TMA boxes) and fp32 storage."""
-    import torch
-    g, rx, ry = random_case(830 + k + nx, nx=nx, ny=ny, nlev=3, sea=sea)
-    var = np.random.default_rng(19).uniform(0.5, 2.0, (3, ny, nx))
-    gpu, cpu = build_pair(P, g, rx, ry, order=1, k=k, variance=var)
-    f = np.random.default_rng(20).standard_normal((2, 3, ny, nx))
-    if dt == "f32":
-        f = f.astype(np.float32)
-    ft = torch.from_numpy(f).cuda()
-    for name in KINDS:
-        monkeypatch.setenv("RGF_B200_RF1", "line")  # read per apply
-        l0 = gpu.launch_count()
-        got = gpu.apply(getattr(P, name), ft)
-        torch.cuda.synchronize()
-        sweeps = {"GX": 1, "GY": 1, "GXT": 1, "GYT": 1, "V": 2, "VT": 2, "B": 4, "GYGX": 2}[name]
-        assert gpu.launch_count() - l0 == sweeps, (name, gpu.launch_count() - l0)
-        got = got.cpu().numpy()
-        monkeypatch.delenv("RGF_B200_RF1")
-        ref = gpu.apply(getattr(P, name), ft).cpu().numpy()
-        assert np.array_equal(got, ref), (name, relmax(got, ref))
-        want = cpu.apply(getattr(O, name), f.astype(np.float64))
-        assert relmax(got, want) <= (TOL64 if dt == "f64" else TOL32), (name, relmax(got, want))
-        assert np.all(got[:, ~g["mask"]] == 0.0), name
-
 
 
 @pytest.mark.parametrize("nx,dt", [(96, "f64"), (160, "f32"), (64, "f64")])
@@ -559,7 +485,7 @@ def test_few_plane_x_sweep_transposed(P, monkeypatch, nlev, nvar, nx, ny, dt):
     (lanes = rows; x tables built in the transposed frame, closures
     included; odd ny pads the transposed rows to a 16 B pitch): every kind
     against the oracle, in place too, with variance and per-level masks."""
-    monkeypatch.setenv("RGF_B200_XT", "1")  # opt-in, read per sweep
+    monkeypatch.setenv("RGF_B200_XT", "1")  # opt-in, read at operator creation
     g, rx, ry = random_case(990 + nx + nlev, nx=nx, ny=ny, nlev=nlev, sea=0.7)
     var = np.random.default_rng(27).uniform(0.5, 2.0, (nlev, ny, nx))
     gpu, cpu = build_pair(P, g, rx, ry, variance=var)
@@ -576,3 +502,73 @@ def test_few_plane_x_sweep_transposed(P, monkeypatch, nlev, nvar, nx, ny, dt):
     h = f.copy()
     gpu.apply(P.GX, h, out=h)
     assert relmax(h, cpu.apply(O.GX, f.astype(np.float64))) <= tol
+
+
+def test_concurrent_applies_on_two_streams(P):
+    """The reference's apply_* are const and safe to call concurrently
+    (covariance.cpp:21-34, thread_local scratch). Two host threads apply the
+    same operator on two CUDA streams (device fields) and a third thread
+    uses host arrays; the op's shared scratch is event-guarded, so every
+    result equals the oracle's."""
+    import threading
+    import torch
+    g, rx, ry = random_case(77, nx=96, ny=64, nlev=3, sea=0.8)
+    gpu, cpu = build_pair(P, g, rx, ry)
+    rng = np.random.default_rng(78)
+    fields = [rng.standard_normal((2, 3, 64, 96)) for _ in range(3)]
+    kinds = ["GYGX", "VT", "B"]
+    wants = [cpu.apply(getattr(O, k), f) for k, f in zip(kinds, fields)]
+    got = [None] * 3
+    errors = []
+
+    def dev(i):
+        try:
+            s = torch.cuda.Stream()
+            x = torch.from_numpy(fields[i]).cuda()
+            torch.cuda.synchronize()
+            with torch.cuda.stream(s):
+                outs = [gpu.apply(getattr(P, kinds[i]), x) for _ in range(20)]
+            s.synchronize()
+            got[i] = [o.cpu().numpy() for o in outs]
+        except Exception as e:  # pragma: no cover - reported below
+            errors.append(e)
+
+    def host(i):
+        try:
+            got[i] = [gpu.apply(getattr(P, kinds[i]), fields[i]) for _ in range(5)]
+        except Exception as e:  # pragma: no cover
+            errors.append(e)
+
+    ts = [threading.Thread(target=dev, args=(0,)), threading.Thread(target=dev, args=(1,)),
+          threading.Thread(target=host, args=(2,))]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    assert not errors, errors
+    for i in range(3):
+        for r in got[i]:
+            assert relmax(r, wants[i]) <= TOL64, (kinds[i], relmax(r, wants[i]))
+
+
+def test_apply_out_argument_is_checked(P):
+    """A caller-supplied `out` must match the field's dtype, shape and layout
+    (and device for tensors): the C ABI writes field-sized data through it."""
+    import torch
+    g, rx, ry = random_case(79, nx=64, ny=40, nlev=1)
+    gpu, _ = build_pair(P, g, rx, ry)
+    f = np.random.default_rng(80).standard_normal((1, 1, 40, 64))
+    with pytest.raises(P.InvalidArgument):
+        gpu.apply(P.GYGX, f, out=np.empty(f.shape, np.float32))
+    with pytest.raises(P.InvalidArgument):
+        gpu.apply(P.GYGX, f, out=np.empty((1, 1, 40, 32)))
+    with pytest.raises(P.InvalidArgument):
+        gpu.apply(P.GYGX, f, out=np.empty((1, 1, 64, 40)).transpose(0, 1, 3, 2))
+    t = torch.from_numpy(f).cuda()
+    with pytest.raises(P.InvalidArgument):
+        gpu.apply(P.GYGX, t, out=torch.empty_like(t, dtype=torch.float32))
+    with pytest.raises(P.InvalidArgument):
+        gpu.apply(P.GYGX, t, out=torch.empty((1, 1, 64, 40), dtype=t.dtype,
+                                             device="cuda").transpose(2, 3))
+    ok = np.empty_like(f)
+    assert gpu.apply(P.GYGX, f, out=ok) is ok
