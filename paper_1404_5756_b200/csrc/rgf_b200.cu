@@ -24,6 +24,7 @@
 #include "sweep_stream.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_ckpt.cuh"
+#include "sweep_sp.cuh"
 #include "rf1_stream.cuh"
 #include "closures.cuh"
 #include "solver_kernels.cuh"
@@ -138,6 +139,13 @@ struct rgf_op {
   bool stream_ok = false;
   bool ckpt_ok = true;  // TMA-fed sweeps (checkpointed / single-pass) for this op's tables
   bool xt_env = false;   // RGF_B200_XT=1 at creation: few-plane x sweeps on the transposed field
+  // single-pass x sweeps (sweep_sp.cuh): one mask class (every level's mask
+  // identical) and one ghost width; tables per part (forward / adjoint)
+  bool one_mask = false;
+  int sp_mode = 1;  // RGF_B200_SP at creation: 0 off, 1 on (default)
+  int sp_rw = 0, sp_rc = 0, sp_cs = 0;
+  bool sp_built[2] = {false, false};
+  DevBuf<double> sp_tab[2], sp_chk[2], sp_ccta[2], sp_cl[2];
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
@@ -276,6 +284,80 @@ void build_xt(rgf_op* op, cudaStream_t st) {
   op->xt_ok = true;
 }
 
+rgfb::XspArgs xsp_args(const rgf_op* op, int part) {
+  rgfb::XspArgs a{};
+  a.nx = op->nx;
+  a.ny = op->ny;
+  a.nh = op->nx * op->ny;
+  a.pitch = op->nx;
+  a.RW = op->sp_rw;
+  a.RC = op->sp_rc;
+  a.CS = op->sp_cs;
+  a.words = op->words[0];
+  a.bits = op->bits[0].p;  // level 0 stands for the single mask class
+  a.ghosts = op->ghost[0] > 0;
+  a.c3 = op->dx_.c3.p;
+  a.ipitch = (op->nx + 1) / 2 * 2;
+  a.idc = !op->unit_dc ? nullptr : (a.ipitch == op->nx ? op->dx_.idc.p : op->dx_.idcp.p);
+  a.clos = op->clos.p + rgfb::clos_off(0, 0, part, a.nh, 0);
+  a.tab = op->sp_tab[part].p;
+  a.chk = op->sp_chk[part].p;
+  a.ccta = op->sp_ccta[part].p;
+  a.cl = op->sp_cl[part].p;
+  return a;
+}
+
+// Single-pass x sweep (sweep_sp.cuh); false if it cannot run here (the
+// caller then takes the checkpointed kernels).
+bool sp_x(rgf_op* op, bool transpose, const double* in, double* out, int64_t nvar, int64_t lev0,
+          int64_t nlev, int64_t pitch, const double* pre, const double* post, cudaStream_t st) {
+  const int part = transpose ? 1 : 0;
+  if (!op->sp_built[part]) {
+    int rw = 0, rc = 0, cs = 0;
+    if (!rgfb::xsp_chunking(op->nx, rw, rc, cs)) {
+      op->sp_mode = 0;
+      return false;
+    }
+    op->sp_rw = rw;
+    op->sp_rc = rc;
+    op->sp_cs = cs;
+    const int64_t nh = op->nx * op->ny;
+    const int64_t nchunk = op->ny * cs;
+    op->sp_tab[part].alloc(static_cast<size_t>(nh * 6));
+    op->sp_chk[part].alloc(static_cast<size_t>(nchunk * rgfb::sp::NW * rgfb::sp::CHKW));
+    op->sp_ccta[part].alloc(static_cast<size_t>(nchunk * rgfb::sp::CHKW));
+    op->sp_cl[part].alloc(static_cast<size_t>(nchunk * rgfb::sp::NW * rgfb::sp::MAXE * 10));
+    CUDA_OK(cudaMemsetAsync(op->sp_cl[part].p, 0, op->sp_cl[part].bytes(), st));
+    const rgfb::XspArgs a = xsp_args(op, part);
+    if (transpose)
+      rgfb::k_xsp_tables<true><<<grid_for(nchunk, 64), 64, 0, st>>>(
+          a, op->sp_tab[part].p, op->sp_chk[part].p, op->sp_ccta[part].p, op->sp_cl[part].p);
+    else
+      rgfb::k_xsp_tables<false><<<grid_for(nchunk, 64), 64, 0, st>>>(
+          a, op->sp_tab[part].p, op->sp_chk[part].p, op->sp_ccta[part].p, op->sp_cl[part].p);
+    CUDA_OK(cudaGetLastError());
+    op->sp_built[part] = true;
+  }
+  rgfb::XspArgs a = xsp_args(op, part);
+  a.pitch = pitch;
+  a.planes = nvar * nlev;
+  a.nlev = nlev;
+  a.lev0 = lev0;
+  a.PB = static_cast<int>((a.planes + 31) / 32);
+  a.ppc = static_cast<int>((a.planes + a.PB - 1) / a.PB);
+  a.pre_scale = pre;
+  a.post_scale = post;
+  if (a.ny * a.PB * a.CS >= (int64_t(1) << 31)) return false;
+  if (!rgfb::launch_xsp(in, out, a, transpose, op->unit_dc != 0, pre != nullptr, post != nullptr,
+                        st)) {
+    cudaGetLastError();  // clear: fall back to the checkpointed kernels from now on
+    op->sp_mode = 0;
+    return false;
+  }
+  op->launches += 1;
+  return true;
+}
+
 template <typename T>
 void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nvar,
            int64_t lev0, int64_t nlev, const double* pre, const double* post, cudaStream_t st,
@@ -321,6 +403,11 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     // (RGF_B200_XT=1, read per sweep): 1024^2 single level 2x faster, C3
     // level 0 slower (one plane leaves 7 of the y CTA's 8 plane-warps idle),
     // DESIGN §10.
+    if (dir == 0 && sizeof(T) == 8 && op->sp_mode && op->one_mask && op->nclass == 1 &&
+        rgfb::tma_supported(in, out, pitch) &&
+        sp_x(op, transpose, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(out),
+             nvar, lev0, nlev, pitch, pre, post, st))
+      return;
     if (op->xt_env && dir == 0 && op->ckpt_ok && nvar * nlev <= 8 && !pre && !post &&
         rgfb::tma_supported(in, out, pitch)) {
       if (!op->xt_ok) build_xt(op, st);
@@ -949,6 +1036,10 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
         CUDA_OK(cudaDeviceSynchronize());
         op->stream_ok = true;
+        op->one_mask = true;
+        for (int64_t l = 1; l < g->nlev && op->one_mask; ++l)
+          op->one_mask = std::memcmp(g->mask, g->mask + l * nh, static_cast<size_t>(nh)) == 0;
+        if (const char* e = std::getenv("RGF_B200_SP")) op->sp_mode = e[0] == '0' ? 0 : 1;
         const char* xte = std::getenv("RGF_B200_XT");
         op->xt_env = xte && xte[0] == '1';
         if (op->ckpt_ok) {
