@@ -141,14 +141,43 @@ int rgf_rf3_filter_scalars(double sigma, int calibration, double out[5]);
 /* rf1.hpp:76-85 rf1_coefficients -> {alpha, beta} */
 int rgf_rf1_coefficients(double sigma, int k, double out[2]);
 
-/* 1-D entry points rf3_apply_1d / rf3_apply_transpose_1d (rf3.hpp:318-334)
- * and rf1_apply_1d / rf1_apply_transpose_1d (rf1.hpp:475-491) over a batch
- * of `nlines` contiguous host vectors of length m, with per-point sigma
- * (m doubles, shared by the batch) turned into coefficients on the device. */
+/* rf3.hpp:101-108 rf3_cascade_variance(q) */
+int rgf_rf3_cascade_variance(double q, double* out);
+/* rf3.hpp:143-154 rf3_length_scale_argument(sigma, calibration) */
+int rgf_rf3_length_scale_argument(double sigma, int calibration, double* out);
+
+/* 1-D entry points over a batch of `nlines` contiguous host vectors of
+ * length m (one coefficient table, shared by the batch).
+ *
+ * Per-point sigma (m doubles) turned into coefficients on the device:
+ * rf3_apply_1d / rf3_apply_transpose_1d (rf3.hpp:318-334 with
+ * rf3_filter_coefficients, rf3.hpp:191-210) and rf1_apply_1d /
+ * rf1_apply_transpose_1d (rf1.hpp:139-155 with the table overload of
+ * rf1_coefficients, rf1.hpp:96-110). */
 int rgf_rf3_apply_1d(const double* in, const double* sigma, int64_t m, int64_t nlines,
                      int calibration, int transpose, double* out);
 int rgf_rf1_apply_1d(const double* in, const double* sigma, int64_t m, int64_t nlines,
                      int k, int transpose, double* out);
+
+/* Coefficient tables (the reference's Rf3CoefficientsT / Rf1CoefficientsT):
+ * rf3_filter_coefficients(sigma, calibration) (rf3.hpp:191-210) and the
+ * table overload rf1_coefficients(sigma, k) (rf1.hpp:96-110), m points. */
+int rgf_rf3_filter_coefficients(const double* sigma, int64_t m, int calibration,
+                                double* alpha1, double* alpha2, double* alpha3, double* beta);
+int rgf_rf1_coefficients_table(const double* sigma, int64_t m, int k, double* alpha,
+                               double* beta);
+
+/* Filters with caller-supplied tables: rf3_filter_in_place /
+ * rf3_filter_transpose_in_place / rf3_apply_1d(segment, coefficients)
+ * (rf3.hpp:292-334) and rf1_filter_in_place / rf1_filter_transpose_in_place /
+ * rf1_apply_1d(segment, coefficients) (rf1.hpp:113-155). `in` may equal
+ * `out` (in place). Errors as the reference: "rf3 filter: segment length must
+ * be >= 4", "rf1 filter: segment length must be >= 2". */
+int rgf_rf3_filter(const double* in, const double* alpha1, const double* alpha2,
+                   const double* alpha3, const double* beta, int64_t m, int64_t nlines,
+                   int transpose, double* out);
+int rgf_rf1_filter(const double* in, const double* alpha, const double* beta, int64_t m,
+                   int64_t nlines, int k, int transpose, double* out);
 
 
 /* ------------------------------------------------------------------------

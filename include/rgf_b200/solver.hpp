@@ -13,8 +13,9 @@
 namespace rgf {
 
 #ifdef RGF_B200_USE_EIGEN
-using Vector = Eigen::VectorXd;
-using Positions = Eigen::ArrayX2d;
+}  // namespace rgf
+#include "rgf/obs.hpp"  // the reference's ObsSet, obs_operator(_transpose), misfit (obs.cpp)
+namespace rgf {
 #else
 // column vector (Eigen::VectorXd stand-in)
 class Vector {
@@ -33,7 +34,6 @@ class Vector {
 };
 // n x 2 column-major positions (Eigen::ArrayX2d stand-in): (n, 0) = x, (n, 1) = y
 using Positions = Array2<Scalar>;
-#endif
 
 // obs.hpp:15-25
 struct ObsSet {
@@ -42,6 +42,7 @@ struct ObsSet {
   Vector r_var;
   Index size() const { return values.size(); }
 };
+#endif
 
 // solver.hpp:19-40
 struct SolveOptions {
@@ -103,6 +104,7 @@ class DeviceObs {
 inline const double* flat(const Field& f) { return f.data(); }
 }  // namespace detail
 
+#ifndef RGF_B200_USE_EIGEN  // the drop-in keeps the reference's obs.cpp for these
 // obs.hpp:41-43: H, bilinear interpolation at each observation
 inline Vector obs_operator(const StateField& field, const ObsSet& obs) {
   if (!field.grid) throw std::invalid_argument("obs_operator: field has no grid");
@@ -135,6 +137,8 @@ inline Vector misfit(const Vector& background_at_obs, const ObsSet& obs) {
   for (Index k = 0; k < obs.size(); ++k) d[k] = obs.values[k] - background_at_obs[k];
   return d;
 }
+
+#endif
 
 // solver.hpp:45-47
 inline CostReport cost(const StateField& chi, const ObsSet& obs, const HorizontalCovarianceOp& op,

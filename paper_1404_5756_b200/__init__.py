@@ -28,6 +28,8 @@ __all__ = [
     "CovarianceOptions", "HorizontalCovarianceOp", "InvalidArgument", "DeviceError",
     "rf3_coefficients", "rf3_filter_scalars", "rf1_coefficients",
     "rf3_apply_1d", "rf3_apply_transpose_1d", "rf1_apply_1d", "rf1_apply_transpose_1d",
+    "rf3_cascade_variance", "rf3_length_scale_argument", "Rf3Coefficients", "Rf1Coefficients",
+    "rf3_filter_coefficients", "rf1_coefficients_table", "rf3_filter", "rf1_filter",
     "lib", "LIB_PATH",
 ]
 
@@ -76,6 +78,12 @@ lib.rgf_rf3_filter_scalars.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
 lib.rgf_rf1_coefficients.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
 lib.rgf_rf3_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
 lib.rgf_rf1_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
+lib.rgf_rf3_cascade_variance.argtypes = [ctypes.c_double, _dp]
+lib.rgf_rf3_length_scale_argument.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
+lib.rgf_rf3_filter_coefficients.argtypes = [_vp, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]
+lib.rgf_rf1_coefficients_table.argtypes = [_vp, _i64, ctypes.c_int, _vp, _vp]
+lib.rgf_rf3_filter.argtypes = [_vp, _vp, _vp, _vp, _vp, _i64, _i64, ctypes.c_int, _vp]
+lib.rgf_rf1_filter.argtypes = [_vp, _vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
 
 # C ABI constants (include/rgf_b200.h)
 GX, GY, GXT, GYT, V, VT, B, GYGX = range(8)
@@ -389,7 +397,7 @@ class Rf3Scalars:  # rf3.hpp:159-164
 
 
 @dataclass
-class Rf1Scalars:  # rf1.hpp:403-407
+class Rf1Scalars:  # rf1.hpp:66-70
     alpha: float
     beta: float
 
@@ -433,12 +441,85 @@ def rf3_apply_transpose_1d(x, sigma, calibration=Rf3Calibration.yvv95):
 
 
 def rf1_apply_1d(x, sigma, k):
-    """rf1.hpp:475-482 with rf1_coefficients(sigma, k) (rf1.hpp:432-446)."""
+    """rf1.hpp:139-146 with rf1_coefficients(sigma, k) (rf1.hpp:96-110)."""
     return _apply_1d(lib.rgf_rf1_apply_1d, x, sigma, int(k), 0)
 
 
 def rf1_apply_transpose_1d(x, sigma, k):
     return _apply_1d(lib.rgf_rf1_apply_1d, x, sigma, int(k), 1)
+
+
+def rf3_cascade_variance(q: float) -> float:
+    """rf3.hpp:101-108."""
+    out = ctypes.c_double()
+    _check(lib.rgf_rf3_cascade_variance(float(q), ctypes.byref(out)))
+    return out.value
+
+
+def rf3_length_scale_argument(sigma: float, calibration: Rf3Calibration) -> float:
+    """rf3.hpp:143-154."""
+    out = ctypes.c_double()
+    _check(lib.rgf_rf3_length_scale_argument(float(sigma), int(calibration), ctypes.byref(out)))
+    return out.value
+
+
+@dataclass
+class Rf3Coefficients:  # rf3.hpp:183-189 (Rf3CoefficientsT)
+    alpha1: np.ndarray
+    alpha2: np.ndarray
+    alpha3: np.ndarray
+    beta: np.ndarray
+
+
+@dataclass
+class Rf1Coefficients:  # rf1.hpp:87-92 (Rf1CoefficientsT)
+    alpha: np.ndarray
+    beta: np.ndarray
+    k_iterations: int = 1
+
+
+def rf3_filter_coefficients(sigma, calibration=Rf3Calibration.yvv95) -> Rf3Coefficients:
+    """rf3.hpp:191-210: per-point tables from a sigma array (device)."""
+    sig = np.ascontiguousarray(sigma, dtype=np.float64).ravel()
+    t = [np.empty_like(sig) for _ in range(4)]
+    _check(lib.rgf_rf3_filter_coefficients(_ptr(sig), sig.size, int(calibration),
+                                           *(_ptr(a) for a in t)))
+    return Rf3Coefficients(*t)
+
+
+def rf1_coefficients_table(sigma, k) -> Rf1Coefficients:
+    """rf1.hpp:96-110: the table overload of rf1_coefficients (device)."""
+    sig = np.ascontiguousarray(sigma, dtype=np.float64).ravel()
+    a, b = np.empty_like(sig), np.empty_like(sig)
+    _check(lib.rgf_rf1_coefficients_table(_ptr(sig), sig.size, int(k), _ptr(a), _ptr(b)))
+    return Rf1Coefficients(a, b, int(k))
+
+
+def _filter_tables(x, m, fn, tabs, *args):
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    if x.shape[-1] != m or any(np.size(t) != m for t in tabs):
+        raise InvalidArgument("rf filter: coefficient length mismatch")
+    tabs = [np.ascontiguousarray(t, dtype=np.float64) for t in tabs]
+    out = np.empty_like(x)
+    nlines = x.size // m if m else 0
+    _check(fn(_ptr(x), *(_ptr(t) for t in tabs), m, max(nlines, 1), *args, _ptr(out)))
+    return out
+
+
+def rf3_filter(x, c: Rf3Coefficients, transpose=False):
+    """rf3_filter_in_place / _transpose_in_place / rf3_apply_1d(segment, c)
+    (rf3.hpp:292-334) over the last axis of x, with caller tables."""
+    x = np.asarray(x, dtype=np.float64)
+    return _filter_tables(x, x.shape[-1], lib.rgf_rf3_filter,
+                          (c.alpha1, c.alpha2, c.alpha3, c.beta), int(bool(transpose)))
+
+
+def rf1_filter(x, c: Rf1Coefficients, transpose=False):
+    """rf1_filter_in_place / _transpose_in_place / rf1_apply_1d(segment, c)
+    (rf1.hpp:113-155) over the last axis of x, with caller tables."""
+    x = np.asarray(x, dtype=np.float64)
+    return _filter_tables(x, x.shape[-1], lib.rgf_rf1_filter, (c.alpha, c.beta),
+                          int(c.k_iterations), int(bool(transpose)))
 
 
 # --------------------------------------------------------------------------

@@ -24,7 +24,6 @@
 #include "sweep_stream.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_ckpt.cuh"
-#include "sweep_sp.cuh"
 #include "rf1_stream.cuh"
 #include "closures.cuh"
 #include "solver_kernels.cuh"
@@ -139,13 +138,6 @@ struct rgf_op {
   bool stream_ok = false;
   bool ckpt_ok = true;  // TMA-fed sweeps (checkpointed / single-pass) for this op's tables
   bool xt_env = false;   // RGF_B200_XT=1 at creation: few-plane x sweeps on the transposed field
-  // single-pass x sweeps (sweep_sp.cuh): one mask class (every level's mask
-  // identical) and one ghost width; tables per part (forward / adjoint)
-  bool one_mask = false;
-  int sp_mode = 1;  // RGF_B200_SP at creation: 0 off, 1 on (default)
-  int sp_rw = 0, sp_rc = 0, sp_cs = 0;
-  bool sp_built[2] = {false, false};
-  DevBuf<double> sp_tab[2], sp_chk[2], sp_ccta[2], sp_cl[2];
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
@@ -284,80 +276,6 @@ void build_xt(rgf_op* op, cudaStream_t st) {
   op->xt_ok = true;
 }
 
-rgfb::XspArgs xsp_args(const rgf_op* op, int part) {
-  rgfb::XspArgs a{};
-  a.nx = op->nx;
-  a.ny = op->ny;
-  a.nh = op->nx * op->ny;
-  a.pitch = op->nx;
-  a.RW = op->sp_rw;
-  a.RC = op->sp_rc;
-  a.CS = op->sp_cs;
-  a.words = op->words[0];
-  a.bits = op->bits[0].p;  // level 0 stands for the single mask class
-  a.ghosts = op->ghost[0] > 0;
-  a.c3 = op->dx_.c3.p;
-  a.ipitch = (op->nx + 1) / 2 * 2;
-  a.idc = !op->unit_dc ? nullptr : (a.ipitch == op->nx ? op->dx_.idc.p : op->dx_.idcp.p);
-  a.clos = op->clos.p + rgfb::clos_off(0, 0, part, a.nh, 0);
-  a.tab = op->sp_tab[part].p;
-  a.chk = op->sp_chk[part].p;
-  a.ccta = op->sp_ccta[part].p;
-  a.cl = op->sp_cl[part].p;
-  return a;
-}
-
-// Single-pass x sweep (sweep_sp.cuh); false if it cannot run here (the
-// caller then takes the checkpointed kernels).
-bool sp_x(rgf_op* op, bool transpose, const double* in, double* out, int64_t nvar, int64_t lev0,
-          int64_t nlev, int64_t pitch, const double* pre, const double* post, cudaStream_t st) {
-  const int part = transpose ? 1 : 0;
-  if (!op->sp_built[part]) {
-    int rw = 0, rc = 0, cs = 0;
-    if (!rgfb::xsp_chunking(op->nx, rw, rc, cs)) {
-      op->sp_mode = 0;
-      return false;
-    }
-    op->sp_rw = rw;
-    op->sp_rc = rc;
-    op->sp_cs = cs;
-    const int64_t nh = op->nx * op->ny;
-    const int64_t nchunk = op->ny * cs;
-    op->sp_tab[part].alloc(static_cast<size_t>(nh * 6));
-    op->sp_chk[part].alloc(static_cast<size_t>(nchunk * rgfb::sp::NW * rgfb::sp::CHKW));
-    op->sp_ccta[part].alloc(static_cast<size_t>(nchunk * rgfb::sp::CHKW));
-    op->sp_cl[part].alloc(static_cast<size_t>(nchunk * rgfb::sp::NW * rgfb::sp::MAXE * 10));
-    CUDA_OK(cudaMemsetAsync(op->sp_cl[part].p, 0, op->sp_cl[part].bytes(), st));
-    const rgfb::XspArgs a = xsp_args(op, part);
-    if (transpose)
-      rgfb::k_xsp_tables<true><<<grid_for(nchunk, 64), 64, 0, st>>>(
-          a, op->sp_tab[part].p, op->sp_chk[part].p, op->sp_ccta[part].p, op->sp_cl[part].p);
-    else
-      rgfb::k_xsp_tables<false><<<grid_for(nchunk, 64), 64, 0, st>>>(
-          a, op->sp_tab[part].p, op->sp_chk[part].p, op->sp_ccta[part].p, op->sp_cl[part].p);
-    CUDA_OK(cudaGetLastError());
-    op->sp_built[part] = true;
-  }
-  rgfb::XspArgs a = xsp_args(op, part);
-  a.pitch = pitch;
-  a.planes = nvar * nlev;
-  a.nlev = nlev;
-  a.lev0 = lev0;
-  a.PB = static_cast<int>((a.planes + 31) / 32);
-  a.ppc = static_cast<int>((a.planes + a.PB - 1) / a.PB);
-  a.pre_scale = pre;
-  a.post_scale = post;
-  if (a.ny * a.PB * a.CS >= (int64_t(1) << 31)) return false;
-  if (!rgfb::launch_xsp(in, out, a, transpose, op->unit_dc != 0, pre != nullptr, post != nullptr,
-                        st)) {
-    cudaGetLastError();  // clear: fall back to the checkpointed kernels from now on
-    op->sp_mode = 0;
-    return false;
-  }
-  op->launches += 1;
-  return true;
-}
-
 template <typename T>
 void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nvar,
            int64_t lev0, int64_t nlev, const double* pre, const double* post, cudaStream_t st,
@@ -403,11 +321,6 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     // (RGF_B200_XT=1, read per sweep): 1024^2 single level 2x faster, C3
     // level 0 slower (one plane leaves 7 of the y CTA's 8 plane-warps idle),
     // DESIGN §10.
-    if (dir == 0 && sizeof(T) == 8 && op->sp_mode && op->one_mask && op->nclass == 1 &&
-        rgfb::tma_supported(in, out, pitch) &&
-        sp_x(op, transpose, reinterpret_cast<const double*>(in), reinterpret_cast<double*>(out),
-             nvar, lev0, nlev, pitch, pre, post, st))
-      return;
     if (op->xt_env && dir == 0 && op->ckpt_ok && nvar * nlev <= 8 && !pre && !post &&
         rgfb::tma_supported(in, out, pitch)) {
       if (!op->xt_ok) build_xt(op, st);
@@ -1036,10 +949,6 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
         CUDA_OK(cudaDeviceSynchronize());
         op->stream_ok = true;
-        op->one_mask = true;
-        for (int64_t l = 1; l < g->nlev && op->one_mask; ++l)
-          op->one_mask = std::memcmp(g->mask, g->mask + l * nh, static_cast<size_t>(nh)) == 0;
-        if (const char* e = std::getenv("RGF_B200_SP")) op->sp_mode = e[0] == '0' ? 0 : 1;
         const char* xte = std::getenv("RGF_B200_XT");
         op->xt_env = xte && xte[0] == '1';
         if (op->ckpt_ok) {
@@ -1304,6 +1213,131 @@ static void apply_1d(const double* in, const double* sigma, int64_t m, int64_t n
   CUDA_OK(cudaGetLastError());
   CUDA_OK(cudaMemcpy(out, dout.p, static_cast<size_t>(m * nlines) * sizeof(double),
                      cudaMemcpyDeviceToHost));
+}
+
+static double scalar_helper(double x, int calibration, int mode) {
+  DevBuf<double> d;
+  d.alloc(1);
+  rgfb::k_scalar_helper<<<1, 32>>>(x, calibration, mode, d.p);
+  CUDA_OK(cudaGetLastError());
+  double h = 0.0;
+  CUDA_OK(cudaMemcpy(&h, d.p, sizeof(double), cudaMemcpyDeviceToHost));
+  return h;
+}
+
+int rgf_rf3_cascade_variance(double q, double* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("rf3_cascade_variance: null argument");
+    *out = scalar_helper(q, RGF_CAL_YVV95, 0);
+  });
+}
+
+int rgf_rf3_length_scale_argument(double sigma, int calibration, double* out) {
+  return guarded([&] {
+    if (!out) throw InvalidArgument("rf3_length_scale_argument: null argument");
+    if (calibration < 0 || calibration > 2) throw InvalidArgument("unknown calibration");
+    *out = scalar_helper(sigma, calibration, 1);
+  });
+}
+
+// rf3.hpp:191-210 / rf1.hpp:96-110: per-point tables on the device
+static void tables_1d(const double* sigma, int64_t m, int order, int k, int calibration,
+                      double* a1, double* a2, double* a3, double* b) {
+  DevBuf<double> sig, t1, t2, t3, t4;
+  DevBuf<rgfb::Coef3> c3;
+  DevBuf<double2> c1;
+  sig.upload(sigma, static_cast<size_t>(m));
+  if (order == 3)
+    c3.alloc(static_cast<size_t>(m));
+  else
+    c1.alloc(static_cast<size_t>(m));
+  for (DevBuf<double>* t : {&t1, &t2, &t3, &t4}) t->alloc(static_cast<size_t>(m));
+  rgfb::k_coefficients_1d<<<grid_for(m, 128), 128>>>(sig.p, m, order, k, calibration, c3.p, c1.p);
+  rgfb::k_unpack_tables_1d<<<grid_for(m, 128), 128>>>(c3.p, c1.p, m, t1.p, t2.p, t3.p, t4.p);
+  CUDA_OK(cudaGetLastError());
+  const size_t bytes = static_cast<size_t>(m) * sizeof(double);
+  CUDA_OK(cudaMemcpy(a1, t1.p, bytes, cudaMemcpyDeviceToHost));
+  if (order == 3) {
+    CUDA_OK(cudaMemcpy(a2, t2.p, bytes, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(a3, t3.p, bytes, cudaMemcpyDeviceToHost));
+  }
+  CUDA_OK(cudaMemcpy(b, t4.p, bytes, cudaMemcpyDeviceToHost));
+}
+
+int rgf_rf3_filter_coefficients(const double* sigma, int64_t m, int calibration, double* alpha1,
+                                double* alpha2, double* alpha3, double* beta) {
+  return guarded([&] {
+    if (m < 0) throw InvalidArgument("rf3_filter_coefficients: negative length");
+    if (m > 0 && (!sigma || !alpha1 || !alpha2 || !alpha3 || !beta))
+      throw InvalidArgument("rf3_filter_coefficients: null argument");
+    if (calibration < 0 || calibration > 2) throw InvalidArgument("unknown calibration");
+    for (int64_t i = 0; i < m; ++i)  // rf3.hpp:170 (rf3_filter_scalars)
+      if (!(sigma[i] > 0)) throw InvalidArgument("rf3_filter_scalars: sigma must be positive");
+    if (m > 0) tables_1d(sigma, m, 3, 1, calibration, alpha1, alpha2, alpha3, beta);
+  });
+}
+
+int rgf_rf1_coefficients_table(const double* sigma, int64_t m, int k, double* alpha,
+                               double* beta) {
+  return guarded([&] {
+    if (m < 0) throw InvalidArgument("rf1_coefficients: negative length");
+    if (m > 0 && (!sigma || !alpha || !beta))
+      throw InvalidArgument("rf1_coefficients: null argument");
+    for (int64_t i = 0; i < m; ++i)  // rf1.hpp:79-80
+      if (!(sigma[i] > 0)) throw InvalidArgument("rf1_coefficients: sigma must be positive");
+    if (k < 1) throw InvalidArgument("rf1_coefficients: k must be >= 1");
+    if (m > 0) tables_1d(sigma, m, 1, k, RGF_CAL_YVV95, alpha, nullptr, nullptr, beta);
+  });
+}
+
+// rf3.hpp:292-334 / rf1.hpp:113-155 with caller tables, one thread per vector
+static void filter_tables_1d(const double* in, const double* a1, const double* a2,
+                             const double* a3, const double* b, int64_t m, int64_t nlines,
+                             int order, int k, int transpose, double* out) {
+  DevBuf<double> t1, t2, t3, t4, din, dout, scr;
+  DevBuf<rgfb::Coef3> c3;
+  DevBuf<double2> c1;
+  t1.upload(a1, static_cast<size_t>(m));
+  t4.upload(b, static_cast<size_t>(m));
+  if (order == 3) {
+    t2.upload(a2, static_cast<size_t>(m));
+    t3.upload(a3, static_cast<size_t>(m));
+    c3.alloc(static_cast<size_t>(m));
+  } else {
+    c1.alloc(static_cast<size_t>(m));
+  }
+  din.upload(in, static_cast<size_t>(m * nlines));
+  dout.alloc(static_cast<size_t>(m * nlines));
+  scr.alloc(static_cast<size_t>(m * nlines));
+  rgfb::k_pack_tables_1d<<<grid_for(m, 128), 128>>>(t1.p, t2.p, t3.p, t4.p, m, c3.p, c1.p);
+  rgfb::k_apply_1d<<<grid_for(nlines, 64, 1 << 20), 64>>>(din.p, dout.p, c3.p, c1.p, m, nlines,
+                                                          order, k, transpose, scr.p);
+  CUDA_OK(cudaGetLastError());
+  CUDA_OK(cudaMemcpy(out, dout.p, static_cast<size_t>(m * nlines) * sizeof(double),
+                     cudaMemcpyDeviceToHost));
+}
+
+int rgf_rf3_filter(const double* in, const double* alpha1, const double* alpha2,
+                   const double* alpha3, const double* beta, int64_t m, int64_t nlines,
+                   int transpose, double* out) {
+  return guarded([&] {
+    if (m < 4) throw InvalidArgument("rf3 filter: segment length must be >= 4");  // rf3.hpp:296
+    if (nlines < 1) throw InvalidArgument("rf3 filter: nlines must be >= 1");
+    if (!in || !alpha1 || !alpha2 || !alpha3 || !beta || !out)
+      throw InvalidArgument("rf3 filter: null argument");
+    filter_tables_1d(in, alpha1, alpha2, alpha3, beta, m, nlines, 3, 1, transpose, out);
+  });
+}
+
+int rgf_rf1_filter(const double* in, const double* alpha, const double* beta, int64_t m,
+                   int64_t nlines, int k, int transpose, double* out) {
+  return guarded([&] {
+    if (m < 2) throw InvalidArgument("rf1 filter: segment length must be >= 2");  // rf1.hpp:117
+    if (nlines < 1) throw InvalidArgument("rf1 filter: nlines must be >= 1");
+    if (k < 1) throw InvalidArgument("rf1_coefficients: k must be >= 1");
+    if (!in || !alpha || !beta || !out) throw InvalidArgument("rf1 filter: null argument");
+    filter_tables_1d(in, alpha, nullptr, nullptr, beta, m, nlines, 1, k, transpose, out);
+  });
 }
 
 int rgf_rf3_apply_1d(const double* in, const double* sigma, int64_t m, int64_t nlines,

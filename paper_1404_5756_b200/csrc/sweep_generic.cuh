@@ -259,7 +259,7 @@ __global__ void k_sweep_generic(const T* __restrict__ in, T* __restrict__ out, S
   }
 }
 
-// 1-D entry points (rf3.hpp:292-334, rf1.hpp:448-491): whole vector, no
+// 1-D entry points (rf3.hpp:292-334, rf1.hpp:113-155): whole vector, no
 // ghosts, per-point coefficient arrays shared by the batch of lines.
 __global__ void k_apply_1d(const double* in, double* out, const Coef3* c3, const double2* c1,
                            int64_t m, int64_t nlines, int order, int k, int transpose,
@@ -302,6 +302,41 @@ __global__ void k_coefficients_1d(const double* sigma, int64_t m, int order, int
     } else {
       const Scal3 f = rf3_filter_scalars(sigma[p], calibration);
       c3[p] = Coef3{f.alpha1, f.alpha2, f.alpha3, f.beta};
+    }
+  }
+}
+
+// caller-supplied tables -> the device layouts k_apply_1d reads
+__global__ void k_pack_tables_1d(const double* a1, const double* a2, const double* a3,
+                                 const double* b, int64_t m, Coef3* c3, double2* c1) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    if (c3) c3[p] = Coef3{a1[p], a2[p], a3[p], b[p]};
+    if (c1) c1[p] = make_double2(a1[p], b[p]);
+  }
+}
+
+// scalar helpers: out[0] = rf3_cascade_variance(x) (mode 0) or
+// rf3_length_scale_argument(x, calibration) (mode 1)
+__global__ void k_scalar_helper(double x, int calibration, int mode, double* out) {
+  if (threadIdx.x != 0) return;
+  out[0] = mode == 0 ? rf3_cascade_variance(x) : rf3_length_scale_argument(x, calibration);
+}
+
+// coefficient tables of m points, unpacked (rf3_filter_coefficients /
+// rf1_coefficients table overload)
+__global__ void k_unpack_tables_1d(const Coef3* c3, const double2* c1, int64_t m, double* a1,
+                                   double* a2, double* a3, double* b) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < m;
+       p += (int64_t)gridDim.x * blockDim.x) {
+    if (c3) {
+      a1[p] = c3[p].a1;
+      a2[p] = c3[p].a2;
+      a3[p] = c3[p].a3;
+      b[p] = c3[p].b;
+    } else {
+      a1[p] = c1[p].x;
+      b[p] = c1[p].y;
     }
   }
 }

@@ -572,3 +572,50 @@ def test_apply_out_argument_is_checked(P):
                                              device="cuda").transpose(2, 3))
     ok = np.empty_like(f)
     assert gpu.apply(P.GYGX, f, out=ok) is ok
+
+
+def test_1d_entry_points_with_coefficient_tables(P):
+    """rf3_filter_coefficients / the rf1 table overload (rf3.hpp:191-210,
+    rf1.hpp:96-110) and the filters taking those tables (rf3.hpp:292-334,
+    rf1.hpp:113-155): tables match the oracle's per-point builders, filtering
+    with them equals the sigma entry points bit for bit and the oracle within
+    1e-14 of the output scale; the scalar helpers rf3_cascade_variance and
+    rf3_length_scale_argument (rf3.hpp:101-154) match the oracle."""
+    rng = np.random.default_rng(31)
+    m = 97
+    sig = rng.uniform(0.8, 9.5, m)
+    x = rng.standard_normal((5, m))
+    for cal in (0, 1, 2):
+        c = P.rf3_filter_coefficients(sig, P.Rf3Calibration(cal))
+        for i in (0, 17, 96):
+            s = O.rf3_filter_scalars(sig[i], cal)  # alpha1 alpha2 alpha3 beta q
+            got_a = np.array([c.alpha1[i], c.alpha2[i], c.alpha3[i], c.beta[i]])
+            assert np.all(np.abs(got_a - s[:4]) <= 4 * np.spacing(np.abs(s[:4]))), (cal, i)
+        for tr in (False, True):
+            got = P.rf3_filter(x, c, transpose=tr)
+            if cal == 0:
+                same = (P.rf3_apply_transpose_1d if tr else P.rf3_apply_1d)(x, sig)
+                assert np.array_equal(got, same)
+            for r in range(5):
+                want = O.rf3_apply_1d_coeffs(x[r], c.alpha1, c.alpha2, c.alpha3, c.beta,
+                                             transpose=tr)
+                assert relmax(got[r], want) <= 1e-14
+    for k in (1, 4):
+        c1 = P.rf1_coefficients_table(sig, k)
+        for i in (0, 50):
+            s1 = O.rf1_coefficients(sig[i], k)
+            assert c1.alpha[i] == s1[0] and c1.beta[i] == s1[1]
+        for tr in (False, True):
+            got = P.rf1_filter(x, c1, transpose=tr)
+            same = (P.rf1_apply_transpose_1d if tr else P.rf1_apply_1d)(x, sig, k)
+            assert np.array_equal(got, same)
+    for q in (0.5, 2.0, 7.5):
+        assert P.rf3_cascade_variance(q) == pytest.approx(O.rf3_cascade_variance(q), rel=1e-14)
+    for s0 in (0.3, 2.0, 8.0):
+        for cal in (0, 1, 2):
+            assert P.rf3_length_scale_argument(s0, P.Rf3Calibration(cal)) == pytest.approx(
+                O.rf3_length_scale_argument(s0, cal), rel=1e-13)
+    with pytest.raises(P.InvalidArgument, match="segment length must be >= 4"):
+        P.rf3_filter(np.zeros(3), P.rf3_filter_coefficients(np.ones(3)))
+    with pytest.raises(P.InvalidArgument, match="sigma must be positive"):
+        P.rf3_filter_coefficients(np.array([1.0, -1.0]))
