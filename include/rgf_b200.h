@@ -181,6 +181,36 @@ int rgf_rf1_filter(const double* in, const double* alpha, const double* beta, in
 
 
 /* ------------------------------------------------------------------------
+ * Container I/O (io.cpp:133-281, proj/README.md "File
+ * formats"): rgf-grid / rgf-scale / rgf-field binary containers (one JSON
+ * header line, then raw little-endian f64 sections in header order, x
+ * fastest; masks one byte per point). Errors: RGF_ERUNTIME with io.cpp's
+ * messages ("cannot open <path>", "expected a \"rgf-field\" container",
+ * "field file dimensions do not match the grid", "payload section \"values\"
+ * is truncated (dimension mismatch?)", ...), RGF_EINVAL for grid.cpp's
+ * validation. Headers are written as nlohmann::json::dump() writes them, so
+ * a save/load round trip is byte-identical. */
+/* header of any container: format (<= 31 chars + NUL), nx, ny, ghost_width
+ * (0 if absent), nlev (1 if absent; rgf-field level stacks, an extension) */
+int rgf_container_info(const char* path, char* format, int64_t* nx, int64_t* ny,
+                       int64_t* ghost_width, int64_t* nlev);
+/* rgf-grid -> caller buffers (nx*ny each); validated as Grid2D::validate */
+int rgf_grid_load(const char* path, int64_t nx, int64_t ny, double* dx, double* dy,
+                  uint8_t* mask, int64_t* ghost_width);
+int rgf_grid_save(const char* path, const rgf_grid_desc* grid); /* level 0 of the mask */
+/* rgf-scale -> rx, ry (nx*ny each), validated against the grid (grid.cpp:40-55) */
+int rgf_scale_load(const char* path, const rgf_grid_desc* grid, double* rx, double* ry);
+int rgf_scale_save(const char* path, int64_t nx, int64_t ny, const double* rx, const double* ry);
+/* rgf-field (nlev levels) streamed straight into / out of `memory`
+ * (RGF_HOST or RGF_DEVICE, the latter through two pinned chunks overlapping
+ * the file I/O with the copies on `stream`); dtype RGF_F32 converts on the
+ * device (payloads are f64). */
+int rgf_field_load(const char* path, int64_t nx, int64_t ny, int64_t nlev, int dtype, void* dst,
+                   int memory, void* stream);
+int rgf_field_save(const char* path, int64_t nx, int64_t ny, int64_t nlev, int dtype,
+                   const void* src, int memory, void* stream);
+
+/* ------------------------------------------------------------------------
  * Observation operator and 3D-VAR analysis, on an
  * operator with one level. Replaces obs.hpp:15-46 (ObsSet, obs_operator,
  * obs_operator_transpose, misfit) and solver.hpp:19-55 (SolveOptions,

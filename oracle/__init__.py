@@ -58,6 +58,13 @@ lib.rgfo_cost.argtypes = [_vp, _vp, _vp, _vp, _vp, _vp]
 lib.rgfo_solve.argtypes = [_vp, _vp, _d, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, _vp]
 lib.rgfo_op_uniform.argtypes = [_vp, _i64, ctypes.c_int]
 lib.rgfo_resolve_thread_count.argtypes = [ctypes.c_int]
+lib.rgfo_io_last_error.restype = ctypes.c_char_p
+lib.rgfo_load_grid.argtypes = [ctypes.c_char_p, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_i64)]
+lib.rgfo_save_grid.argtypes = [ctypes.c_char_p, _i64, _i64, _i64, _vp, _vp, _vp]
+lib.rgfo_load_scale.argtypes = [ctypes.c_char_p, _i64, _i64, _vp, _vp]
+lib.rgfo_save_scale.argtypes = [ctypes.c_char_p, _i64, _i64, _vp, _vp]
+lib.rgfo_load_field.argtypes = [ctypes.c_char_p, _i64, _i64, _vp]
+lib.rgfo_save_field.argtypes = [ctypes.c_char_p, _i64, _i64, _vp]
 
 GX, GY, GXT, GYT, V, VT, B, GYGX = range(8)
 
@@ -238,3 +245,51 @@ class OracleObs:
         return {"increment": inc, "misfit": mis[:self.n], "cg_iterations": int(info[0]),
                 "converged": bool(info[1]), "gradient_norms": gn[:int(info[2])],
                 "final_relative_residual": out3[0], "j_background": out3[1], "j_obs": out3[2]}
+
+
+# ---------------------------------------------------------------- container I/O
+# io.cpp:133-281 restated with nlohmann::json (rgf_oracle_io.cpp). Arrays are
+# (ny, nx), x fastest, as in the containers.
+def _io_check(status):
+    if status != 0:
+        raise OracleError(lib.rgfo_io_last_error().decode())
+
+
+def load_grid(path, nx, ny):
+    dx, dy = np.empty((ny, nx)), np.empty((ny, nx))
+    mask = np.empty((ny, nx), dtype=np.uint8)
+    g = _i64()
+    _io_check(lib.rgfo_load_grid(str(path).encode(), nx, ny, _p(dx), _p(dy), _p(mask),
+                                 ctypes.byref(g)))
+    return dx, dy, mask.astype(bool), g.value
+
+
+def save_grid(path, dx, dy, mask, ghost_width=0):
+    ny, nx = np.shape(dx)
+    arrs = [np.ascontiguousarray(dx, dtype=np.float64), np.ascontiguousarray(dy, dtype=np.float64),
+            np.ascontiguousarray(mask, dtype=np.uint8)]
+    _io_check(lib.rgfo_save_grid(str(path).encode(), nx, ny, int(ghost_width), *(_p(a) for a in arrs)))
+
+
+def load_scale(path, nx, ny):
+    rx, ry = np.empty((ny, nx)), np.empty((ny, nx))
+    _io_check(lib.rgfo_load_scale(str(path).encode(), nx, ny, _p(rx), _p(ry)))
+    return rx, ry
+
+
+def save_scale(path, rx, ry):
+    ny, nx = np.shape(rx)
+    a, b = (np.ascontiguousarray(v, dtype=np.float64) for v in (rx, ry))
+    _io_check(lib.rgfo_save_scale(str(path).encode(), nx, ny, _p(a), _p(b)))
+
+
+def load_field(path, nx, ny):
+    v = np.empty((ny, nx))
+    _io_check(lib.rgfo_load_field(str(path).encode(), nx, ny, _p(v)))
+    return v
+
+
+def save_field(path, values):
+    ny, nx = np.shape(values)
+    v = np.ascontiguousarray(values, dtype=np.float64)
+    _io_check(lib.rgfo_save_field(str(path).encode(), nx, ny, _p(v)))

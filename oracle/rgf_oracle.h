@@ -84,6 +84,17 @@ int rgfo_solve(const rgfo_op* op, const rgfo_obs* o, double tol, int max_iter,
                const double* background, double* increment, double* misfit, double* gnorms,
                int64_t* info, double* out3);
 
+/* io.cpp:133-281 binary containers (rgf_oracle_io.cpp, nlohmann::json) */
+const char* rgfo_io_last_error(void);
+int rgfo_load_grid(const char* path, int64_t nx, int64_t ny, double* dx, double* dy,
+                   uint8_t* mask, int64_t* ghost_width);
+int rgfo_save_grid(const char* path, int64_t nx, int64_t ny, int64_t ghost_width,
+                   const double* dx, const double* dy, const uint8_t* mask);
+int rgfo_load_scale(const char* path, int64_t nx, int64_t ny, double* rx, double* ry);
+int rgfo_save_scale(const char* path, int64_t nx, int64_t ny, const double* rx, const double* ry);
+int rgfo_load_field(const char* path, int64_t nx, int64_t ny, double* values);
+int rgfo_save_field(const char* path, int64_t nx, int64_t ny, const double* values);
+
 #ifdef __cplusplus
 }
 #endif

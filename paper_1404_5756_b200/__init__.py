@@ -30,6 +30,8 @@ __all__ = [
     "rf3_apply_1d", "rf3_apply_transpose_1d", "rf1_apply_1d", "rf1_apply_transpose_1d",
     "rf3_cascade_variance", "rf3_length_scale_argument", "Rf3Coefficients", "Rf1Coefficients",
     "rf3_filter_coefficients", "rf1_coefficients_table", "rf3_filter", "rf1_filter",
+    "container_info", "load_grid", "save_grid", "load_scale_field", "save_scale_field",
+    "load_state_field", "save_state_field", "IOError_",
     "lib", "LIB_PATH",
 ]
 
@@ -79,6 +81,17 @@ lib.rgf_rf1_coefficients.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
 lib.rgf_rf3_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
 lib.rgf_rf1_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
 lib.rgf_rf3_cascade_variance.argtypes = [ctypes.c_double, _dp]
+lib.rgf_container_info.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(_i64),
+                                   ctypes.POINTER(_i64), ctypes.POINTER(_i64),
+                                   ctypes.POINTER(_i64)]
+lib.rgf_grid_load.argtypes = [ctypes.c_char_p, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_i64)]
+lib.rgf_grid_save.argtypes = [ctypes.c_char_p, ctypes.POINTER(_GridDesc)]
+lib.rgf_scale_load.argtypes = [ctypes.c_char_p, ctypes.POINTER(_GridDesc), _vp, _vp]
+lib.rgf_scale_save.argtypes = [ctypes.c_char_p, _i64, _i64, _vp, _vp]
+lib.rgf_field_load.argtypes = [ctypes.c_char_p, _i64, _i64, _i64, ctypes.c_int, _vp,
+                               ctypes.c_int, _vp]
+lib.rgf_field_save.argtypes = [ctypes.c_char_p, _i64, _i64, _i64, ctypes.c_int, _vp,
+                               ctypes.c_int, _vp]
 lib.rgf_rf3_length_scale_argument.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
 lib.rgf_rf3_filter_coefficients.argtypes = [_vp, _i64, ctypes.c_int, _vp, _vp, _vp, _vp]
 lib.rgf_rf1_coefficients_table.argtypes = [_vp, _i64, ctypes.c_int, _vp, _vp]
@@ -520,6 +533,121 @@ def rf1_filter(x, c: Rf1Coefficients, transpose=False):
     x = np.asarray(x, dtype=np.float64)
     return _filter_tables(x, x.shape[-1], lib.rgf_rf1_filter, (c.alpha, c.beta),
                           int(c.k_iterations), int(bool(transpose)))
+
+
+# --------------------------------------------------------------------------
+# Container I/O (io.cpp:133-281). Binary rgf-grid /
+# rgf-scale / rgf-field containers; fields stream straight into device memory
+# when a torch device is requested.
+class IOError_(RuntimeError):
+    """The reference's std::runtime_error from io.cpp (same message text)."""
+
+
+def _io(status):
+    if status == 2:
+        raise IOError_(lib.rgf_last_error().decode())
+    _check(status)
+
+
+def container_info(path) -> dict:
+    fmt = ctypes.create_string_buffer(32)
+    nx, ny, g, nl = _i64(), _i64(), _i64(), _i64()
+    _io(lib.rgf_container_info(str(path).encode(), fmt, ctypes.byref(nx), ctypes.byref(ny),
+                               ctypes.byref(g), ctypes.byref(nl)))
+    return {"format": fmt.value.decode(), "nx": nx.value, "ny": ny.value,
+            "ghost_width": g.value, "nlev": nl.value}
+
+
+def load_grid(path) -> Grid2D:
+    """io.cpp:133-181 load_grid (binary) with Grid2D::validate (grid.cpp:27-39)."""
+    info = container_info(path)
+    nx, ny = info["nx"], info["ny"]
+    if nx < 1 or ny < 1:
+        raise IOError_("container header is missing nx/ny")
+    dx, dy = np.empty((ny, nx)), np.empty((ny, nx))
+    mask = np.empty((ny, nx), dtype=np.uint8)
+    g = _i64()
+    _io(lib.rgf_grid_load(str(path).encode(), nx, ny, _ptr(dx), _ptr(dy), _ptr(mask),
+                          ctypes.byref(g)))
+    return Grid2D(nx, ny, dx, dy, mask.astype(bool), g.value)
+
+
+def _desc(grid: Grid2D):
+    dx = np.ascontiguousarray(grid.dx, dtype=np.float64)
+    dy = np.ascontiguousarray(grid.dy, dtype=np.float64)
+    m = np.ascontiguousarray(np.reshape(grid.mask, (-1, grid.ny, grid.nx))[0], dtype=np.uint8)
+    return _GridDesc(grid.nx, grid.ny, 1, _ptr(dx), _ptr(dy), _ptr(m), int(grid.ghost_width)), \
+        (dx, dy, m)
+
+
+def save_grid(grid: Grid2D, path) -> None:
+    """io.cpp:183-202 save_grid (level 0 of the mask)."""
+    d, keep = _desc(grid)
+    _io(lib.rgf_grid_save(str(path).encode(), ctypes.byref(d)))
+    del keep
+
+
+def load_scale_field(path, grid: Grid2D) -> ScaleField:
+    """io.cpp:204-235 load_scale_field (binary) with ScaleField::validate."""
+    rx, ry = np.empty((grid.ny, grid.nx)), np.empty((grid.ny, grid.nx))
+    d, keep = _desc(grid)
+    _io(lib.rgf_scale_load(str(path).encode(), ctypes.byref(d), _ptr(rx), _ptr(ry)))
+    del keep
+    return ScaleField(rx, ry)
+
+
+def save_scale_field(scales: ScaleField, path) -> None:
+    """io.cpp:237-249."""
+    rx = np.ascontiguousarray(scales.rx, dtype=np.float64)
+    ry = np.ascontiguousarray(scales.ry, dtype=np.float64)
+    ny, nx = rx.shape
+    _io(lib.rgf_scale_save(str(path).encode(), nx, ny, _ptr(rx), _ptr(ry)))
+
+
+def load_state_field(path, grid: Grid2D, nlev: int = 1, dtype=np.float64, device=None):
+    """io.cpp:251-269 load_state_field (binary): (nlev, ny, nx) levels. With
+    `device` (a torch CUDA device) the payload streams into device memory
+    through pinned chunks (no full host copy) and a torch tensor is returned."""
+    dt = F64 if np.dtype(dtype) == np.float64 else F32
+    shape = (nlev, grid.ny, grid.nx) if nlev > 1 else (grid.ny, grid.nx)
+    if device is None:
+        out = np.empty(shape, dtype=np.float64 if dt == F64 else np.float32)
+        _io(lib.rgf_field_load(str(path).encode(), grid.nx, grid.ny, nlev, dt, _ptr(out), HOST,
+                               None))
+        return out
+    import torch
+    out = torch.empty(shape, dtype=torch.float64 if dt == F64 else torch.float32, device=device)
+    st = torch.cuda.current_stream(out.device)
+    _io(lib.rgf_field_load(str(path).encode(), grid.nx, grid.ny, nlev, dt, out.data_ptr(), DEVICE,
+                           st.cuda_stream))
+    return out
+
+
+def save_state_field(values, path) -> None:
+    """io.cpp:271-281 save_state_field; `values` (…, ny, nx) numpy or CUDA
+    torch tensor (streamed out of device memory through pinned chunks)."""
+    try:
+        import torch
+        is_torch = isinstance(values, torch.Tensor)
+    except ImportError:  # pragma: no cover
+        is_torch = False
+    if is_torch:
+        if not values.is_cuda or not values.is_contiguous():
+            raise InvalidArgument("save_state_field: expected a contiguous CUDA tensor")
+        ny, nx = values.shape[-2:]
+        nlev = values.numel() // (nx * ny)
+        dt = F64 if values.dtype == torch.float64 else F32
+        st = torch.cuda.current_stream(values.device)
+        _io(lib.rgf_field_save(str(path).encode(), nx, ny, nlev, dt, values.data_ptr(), DEVICE,
+                               st.cuda_stream))
+        return
+    v = np.ascontiguousarray(values)
+    if v.dtype not in (np.float64, np.float32):
+        v = v.astype(np.float64)
+    ny, nx = v.shape[-2:]
+    nlev = v.size // (nx * ny)
+    _io(lib.rgf_field_save(str(path).encode(), nx, ny, nlev, F64 if v.dtype == np.float64 else F32,
+                           _ptr(v), HOST, None))
 
 
 # --------------------------------------------------------------------------

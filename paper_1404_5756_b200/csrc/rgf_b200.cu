@@ -27,6 +27,7 @@
 #include "rf1_stream.cuh"
 #include "closures.cuh"
 #include "solver_kernels.cuh"
+#include "container_io.cuh"
 
 namespace {
 
@@ -744,9 +745,299 @@ void validate_rvar(const rgf_obs* o) {  // obs.cpp:48-57 (positions checked at c
 
 }  // namespace
 
+namespace {
+
+__global__ void k_f64_to_f32(const double* in, float* out, int64_t n) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = static_cast<float>(in[p]);
+}
+__global__ void k_f32_to_f64(const float* in, double* out, int64_t n) {
+  for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < n;
+       p += (int64_t)gridDim.x * blockDim.x)
+    out[p] = static_cast<double>(in[p]);
+}
+
+// two pinned host slots + events for the streamed field loads/saves
+struct PinnedPair {
+  static constexpr size_t kChunk = size_t(32) << 20;  // bytes per slot
+  void* h[2] = {nullptr, nullptr};
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+  bool used[2] = {false, false};
+  PinnedPair() {
+    for (int b = 0; b < 2; ++b) {
+      CUDA_OK(cudaMallocHost(&h[b], kChunk));
+      CUDA_OK(cudaEventCreateWithFlags(&ev[b], cudaEventDisableTiming));
+    }
+  }
+  ~PinnedPair() {
+    for (int b = 0; b < 2; ++b) {
+      if (ev[b]) cudaEventSynchronize(ev[b]);
+      if (h[b]) cudaFreeHost(h[b]);
+      if (ev[b]) cudaEventDestroy(ev[b]);
+    }
+  }
+  void acquire(int b) {  // slot b's previous copy has finished
+    if (used[b]) CUDA_OK(cudaEventSynchronize(ev[b]));
+    used[b] = true;
+  }
+};
+
+void check_dims(int64_t nx, int64_t ny, int64_t nlev) {
+  if (nx < 1 || ny < 1 || nlev < 1) throw InvalidArgument("container: bad dimensions");
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* rgf_last_error(void) { return g_last_error.c_str(); }
+
+// --------------------------------------------------------- container I/O
+int rgf_container_info(const char* path, char* format, int64_t* nx, int64_t* ny,
+                       int64_t* ghost_width, int64_t* nlev) {
+  return guarded([&] {
+    if (!path) throw InvalidArgument("container: null path");
+    rgfio::File in(path, "rb");
+    std::string line;
+    int c;
+    while ((c = std::fgetc(in.f)) != EOF && c != '\n') line.push_back(static_cast<char>(c));
+    if (line.empty()) throw std::runtime_error("missing container header");
+    const rgfio::Header h = rgfio::parse_header(line);
+    const auto f = h.scalars.find("format");
+    if (format) {
+      const std::string fs = f == h.scalars.end() ? "" : f->second;
+      std::snprintf(format, 32, "%s", fs.c_str());
+    }
+    if (nx) *nx = rgfio::get_int(h, "nx", -1);
+    if (ny) *ny = rgfio::get_int(h, "ny", -1);
+    if (ghost_width) *ghost_width = rgfio::get_int(h, "ghost_width", 0);
+    if (nlev) *nlev = rgfio::get_int(h, "nlev", 1);
+  });
+}
+
+// io.cpp:133-181 load_grid (binary containers) + grid.cpp:27-39 validate
+int rgf_grid_load(const char* path, int64_t nx, int64_t ny, double* dx, double* dy,
+                  uint8_t* mask, int64_t* ghost_width) {
+  return guarded([&] {
+    if (!path || !dx || !dy || !mask) throw InvalidArgument("load_grid: null argument");
+    check_dims(nx, ny, 1);
+    rgfio::File in(path, "rb");
+    const rgfio::Header h = rgfio::read_header(in, "rgf-grid");
+    if (rgfio::get_int(h, "nx", -1) != nx || rgfio::get_int(h, "ny", -1) != ny)
+      throw InvalidArgument("load_grid: buffers do not match the container's nx/ny");
+    const int64_t g = rgfio::get_int(h, "ghost_width", 0);
+    const size_t n = static_cast<size_t>(nx * ny);
+    bool has_dx = false, has_dy = false, has_mask = false;
+    std::vector<uint8_t> raw;
+    for (const std::string& sec : h.sections) {
+      if (sec == "dx") {
+        rgfio::read_exact(in, dx, n * 8, "payload section \"dx\" is truncated (dimension mismatch?)");
+        has_dx = true;
+      } else if (sec == "dy") {
+        rgfio::read_exact(in, dy, n * 8, "payload section \"dy\" is truncated (dimension mismatch?)");
+        has_dy = true;
+      } else if (sec == "mask") {
+        raw.resize(n);
+        rgfio::read_exact(in, raw.data(), n, "mask section is truncated");
+        for (size_t p = 0; p < n; ++p) mask[p] = raw[p] != 0 ? 1 : 0;
+        has_mask = true;
+      } else {
+        throw std::runtime_error("unknown grid section \"" + sec + "\"");
+      }
+    }
+    if (!has_dx || !has_dy) throw std::runtime_error("grid container is missing dx/dy sections");
+    if (!has_mask) std::memset(mask, 1, n);
+    rgfio::expect_eof(in, "trailing bytes after grid payload");
+    if (nx < 4 || ny < 4) throw InvalidArgument("Grid2D: nx and ny must both be >= 4");
+    for (size_t p = 0; p < n; ++p)
+      if (!(dx[p] > 0) || !(dy[p] > 0))
+        throw InvalidArgument("Grid2D: grid spacing must be strictly positive");
+    if (g < 0) throw InvalidArgument("Grid2D: ghost_width must be >= 0");
+    if (ghost_width) *ghost_width = g;
+  });
+}
+
+// io.cpp:183-202 save_grid (level 0 of the mask)
+int rgf_grid_save(const char* path, const rgf_grid_desc* g) {
+  return guarded([&] {
+    if (!path || !g || !g->dx || !g->dy || !g->mask) throw InvalidArgument("save_grid: null argument");
+    check_dims(g->nx, g->ny, 1);
+    const size_t n = static_cast<size_t>(g->nx * g->ny);
+    rgfio::File out(path, "wb");
+    const int64_t gw = g->ghost_width;
+    const std::string hd = rgfio::dump_header("rgf-grid", g->nx, g->ny, &gw, 1, {"dx", "dy", "mask"});
+    rgfio::write_exact(out, hd.data(), hd.size());
+    rgfio::write_exact(out, g->dx, n * 8);
+    rgfio::write_exact(out, g->dy, n * 8);
+    std::vector<uint8_t> raw(n);
+    for (size_t p = 0; p < n; ++p) raw[p] = g->mask[p] ? 1 : 0;
+    rgfio::write_exact(out, raw.data(), n);
+  });
+}
+
+// io.cpp:204-235 load_scale_field (binary) + grid.cpp:40-55 validate
+int rgf_scale_load(const char* path, const rgf_grid_desc* g, double* rx, double* ry) {
+  return guarded([&] {
+    if (!path || !g || !rx || !ry || !g->dx || !g->dy || !g->mask)
+      throw InvalidArgument("load_scale_field: null argument");
+    check_dims(g->nx, g->ny, 1);
+    rgfio::File in(path, "rb");
+    const rgfio::Header h = rgfio::read_header(in, "rgf-scale");
+    if (rgfio::get_int(h, "nx", -1) != g->nx || rgfio::get_int(h, "ny", -1) != g->ny)
+      throw std::runtime_error("scale file dimensions do not match the grid");
+    const size_t n = static_cast<size_t>(g->nx * g->ny);
+    bool has_rx = false, has_ry = false;
+    for (const std::string& sec : h.sections) {
+      if (sec == "rx") {
+        rgfio::read_exact(in, rx, n * 8, "payload section \"rx\" is truncated (dimension mismatch?)");
+        has_rx = true;
+      } else if (sec == "ry") {
+        rgfio::read_exact(in, ry, n * 8, "payload section \"ry\" is truncated (dimension mismatch?)");
+        has_ry = true;
+      } else {
+        throw std::runtime_error("unknown scale section \"" + sec + "\"");
+      }
+    }
+    if (!has_rx) throw std::runtime_error("scale file is missing the zonal (rx) component");
+    if (!has_ry) throw std::runtime_error("scale file is missing the meridional (ry) component");
+    for (int64_t j = 0; j < g->ny; ++j)
+      for (int64_t i = 0; i < g->nx; ++i) {
+        const size_t p = static_cast<size_t>(j * g->nx + i);
+        if (!g->mask[p]) continue;
+        const double sx = rx[p] / g->dx[p], sy = ry[p] / g->dy[p];
+        if (!(rx[p] > 0) || !(ry[p] > 0) || !std::isfinite(sx) || !std::isfinite(sy))
+          throw InvalidArgument("ScaleField: non-positive or non-finite radius at sea point (" +
+                                std::to_string(i) + "," + std::to_string(j) + ")");
+      }
+  });
+}
+
+// io.cpp:237-249 save_scale_field
+int rgf_scale_save(const char* path, int64_t nx, int64_t ny, const double* rx, const double* ry) {
+  return guarded([&] {
+    if (!path || !rx || !ry) throw InvalidArgument("save_scale_field: null argument");
+    check_dims(nx, ny, 1);
+    const size_t n = static_cast<size_t>(nx * ny);
+    rgfio::File out(path, "wb");
+    const std::string hd = rgfio::dump_header("rgf-scale", nx, ny, nullptr, 1, {"rx", "ry"});
+    rgfio::write_exact(out, hd.data(), hd.size());
+    rgfio::write_exact(out, rx, n * 8);
+    rgfio::write_exact(out, ry, n * 8);
+  });
+}
+
+// io.cpp:251-269 load_state_field, streamed into host or device memory
+int rgf_field_load(const char* path, int64_t nx, int64_t ny, int64_t nlev, int dtype, void* dst,
+                   int memory, void* stream) {
+  return guarded([&] {
+    if (!path || !dst) throw InvalidArgument("load_state_field: null argument");
+    if (dtype != RGF_F64 && dtype != RGF_F32) throw InvalidArgument("load_state_field: unknown dtype");
+    if (memory != RGF_HOST && memory != RGF_DEVICE)
+      throw InvalidArgument("load_state_field: unknown memory kind");
+    check_dims(nx, ny, nlev);
+    rgfio::File in(path, "rb");
+    const rgfio::Header h = rgfio::read_header(in, "rgf-field");
+    if (rgfio::get_int(h, "nx", -1) != nx || rgfio::get_int(h, "ny", -1) != ny)
+      throw std::runtime_error("field file dimensions do not match the grid");
+    if (rgfio::get_int(h, "nlev", 1) != nlev)
+      throw std::runtime_error("field file level count does not match");
+    const std::string trunc = "payload section \"values\" is truncated (dimension mismatch?)";
+    const size_t total = static_cast<size_t>(nx * ny * nlev);
+    if (memory == RGF_HOST) {
+      if (dtype == RGF_F64) {
+        rgfio::read_exact(in, dst, total * 8, trunc);
+      } else {
+        std::vector<double> buf(std::min<size_t>(total, size_t(1) << 20));
+        float* d = static_cast<float*>(dst);
+        for (size_t off = 0; off < total; off += buf.size()) {
+          const size_t n = std::min(buf.size(), total - off);
+          rgfio::read_exact(in, buf.data(), n * 8, trunc);
+          for (size_t p = 0; p < n; ++p) d[off + p] = static_cast<float>(buf[p]);
+        }
+      }
+      return;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PinnedPair pp;
+    const size_t per = PinnedPair::kChunk / 8;  // doubles per slot
+    DevBuf<double> stage;
+    if (dtype == RGF_F32) stage.alloc(std::min(per, total));
+    int b = 0;
+    for (size_t off = 0; off < total; off += per, b ^= 1) {
+      const size_t n = std::min(per, total - off);
+      pp.acquire(b);  // the copy out of slot b two chunks ago is done
+      rgfio::read_exact(in, pp.h[b], n * 8, trunc);  // overlaps the previous slot's H2D
+      if (dtype == RGF_F64) {
+        CUDA_OK(cudaMemcpyAsync(static_cast<double*>(dst) + off, pp.h[b], n * 8,
+                                cudaMemcpyHostToDevice, st));
+      } else {
+        CUDA_OK(cudaMemcpyAsync(stage.p, pp.h[b], n * 8, cudaMemcpyHostToDevice, st));
+        k_f64_to_f32<<<grid_for(static_cast<int64_t>(n), 256), 256, 0, st>>>(
+            stage.p, static_cast<float*>(dst) + off, static_cast<int64_t>(n));
+        CUDA_OK(cudaGetLastError());
+      }
+      CUDA_OK(cudaEventRecord(pp.ev[b], st));
+    }
+    CUDA_OK(cudaStreamSynchronize(st));
+  });
+}
+
+// io.cpp:271-281 save_state_field, streamed out of host or device memory
+int rgf_field_save(const char* path, int64_t nx, int64_t ny, int64_t nlev, int dtype,
+                   const void* src, int memory, void* stream) {
+  return guarded([&] {
+    if (!path || !src) throw InvalidArgument("save_state_field: null argument");
+    if (dtype != RGF_F64 && dtype != RGF_F32) throw InvalidArgument("save_state_field: unknown dtype");
+    if (memory != RGF_HOST && memory != RGF_DEVICE)
+      throw InvalidArgument("save_state_field: unknown memory kind");
+    check_dims(nx, ny, nlev);
+    const size_t total = static_cast<size_t>(nx * ny * nlev);
+    rgfio::File out(path, "wb");
+    const std::string hd = rgfio::dump_header("rgf-field", nx, ny, nullptr, nlev, {"values"});
+    rgfio::write_exact(out, hd.data(), hd.size());
+    if (memory == RGF_HOST) {
+      if (dtype == RGF_F64) {
+        rgfio::write_exact(out, src, total * 8);
+      } else {
+        std::vector<double> buf(std::min<size_t>(total, size_t(1) << 20));
+        const float* s = static_cast<const float*>(src);
+        for (size_t off = 0; off < total; off += buf.size()) {
+          const size_t n = std::min(buf.size(), total - off);
+          for (size_t p = 0; p < n; ++p) buf[p] = static_cast<double>(s[off + p]);
+          rgfio::write_exact(out, buf.data(), n * 8);
+        }
+      }
+      return;
+    }
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    PinnedPair pp;
+    const size_t per = PinnedPair::kChunk / 8;
+    DevBuf<double> stage;
+    if (dtype == RGF_F32) stage.alloc(std::min(per, total));
+    auto issue = [&](size_t off, int b) {  // D2H of the chunk at `off` into slot b
+      const size_t n = std::min(per, total - off);
+      if (dtype == RGF_F64) {
+        CUDA_OK(cudaMemcpyAsync(pp.h[b], static_cast<const double*>(src) + off, n * 8,
+                                cudaMemcpyDeviceToHost, st));
+      } else {
+        k_f32_to_f64<<<grid_for(static_cast<int64_t>(n), 256), 256, 0, st>>>(
+            static_cast<const float*>(src) + off, stage.p, static_cast<int64_t>(n));
+        CUDA_OK(cudaGetLastError());
+        CUDA_OK(cudaMemcpyAsync(pp.h[b], stage.p, n * 8, cudaMemcpyDeviceToHost, st));
+      }
+      CUDA_OK(cudaEventRecord(pp.ev[b], st));
+      pp.used[b] = true;
+    };
+    if (total > 0) issue(0, 0);
+    int b = 0;
+    for (size_t off = 0; off < total; off += per, b ^= 1) {
+      if (off + per < total) issue(off + per, b ^ 1);  // next chunk's D2H overlaps this write
+      CUDA_OK(cudaEventSynchronize(pp.ev[b]));
+      rgfio::write_exact(out, pp.h[b], std::min(per, total - off) * 8);
+    }
+  });
+}
 
 #ifdef RGF_RING_PROF
 // development build only: per-section cycle totals of the ring sweeps
