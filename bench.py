@@ -97,7 +97,16 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.rows.append([x.strip() for x in line.split(",")])
+            self.rows.append([x.strip() for x in line.split(",")] + [time.perf_counter()])
+
+    def mark(self, start=True):
+        """Host time of the timed region's start / end: the summary keeps the
+        samples read inside it (the sampler runs from before the warm-up so
+        nvidia-smi's start-up does not eat the region)."""
+        if start:
+            self.t0 = time.perf_counter()
+        else:
+            self.t1 = time.perf_counter()
 
     def __exit__(self, *a):
         if self.proc:
@@ -108,19 +117,25 @@ class ClockSampler:
                 self.proc.kill()
 
     def summary(self):
-        if not self.rows:
+        t0, t1 = getattr(self, "t0", None), getattr(self, "t1", None)
+        rows = self.rows
+        if t0 is not None and t1 is not None:
+            inside = [r for r in rows if t0 <= r[-1] <= t1 + 0.05]
+            rows = inside or rows[-1:]
+        rows = [r[:-1] for r in rows]
+        if not rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
-        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = set()
-        for r in self.rows:
+        for r in rows:
             for i, n in enumerate(names):
                 if len(r) > 5 + i and r[5 + i].lower().startswith("active"):
                     reasons.add(n)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(self.rows)}
+                "samples": len(rows)}
 
 
 def measured_traffic(cfg_name, dtype, order, kernel):
@@ -301,22 +316,24 @@ def main():
     def launches_now():
         return sop.op.launch_count() if sop.op is not None else 0
 
-    for _ in range(args.warmup):
-        step()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    l0 = launches_now()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     with ClockSampler(local) as clk:
+        for _ in range(args.warmup):
+            step()
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
+        l0 = launches_now()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        clk.mark(True)
         e0.record(stream)
         for _ in range(args.steps):
             step()
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark(False)
         if world > 1:
             dist.barrier()
     launches = launches_now() - l0

@@ -181,6 +181,20 @@ int rgf_rf1_filter(const double* in, const double* alpha, const double* beta, in
 
 
 /* ------------------------------------------------------------------------
+ * Batched diagnostics (diagnostics.cpp:69-135), one
+ * device thread per study, host arrays.
+ * impulse_response(sigma[s], order, k, length, calibration) for n studies:
+ * h is n x length (raw response to a Dirac at length/2), and per study
+ * sum_h, err_h_l2, err_h_max (vs the unit-sum sampled Gaussian). */
+int rgf_impulse_responses(const double* sigma, int64_t n, int order, int k, int64_t length,
+                          int calibration, double* h, double* sum_h, double* err_h_l2,
+                          double* err_h_max);
+/* remark1_bound_check(s0[s], sigma[s], order, k, calibration) for n inputs of
+ * length m (s0 is n x m): out4[4*s..] = {lhs, rhs, err_h_l2, holds (0/1)} */
+int rgf_remark1_checks(const double* s0, const double* sigma, int64_t n, int64_t m, int order,
+                       int k, int calibration, double* out4);
+
+/* ------------------------------------------------------------------------
  * Container I/O (io.cpp:133-281, proj/README.md "File
  * formats"): rgf-grid / rgf-scale / rgf-field binary containers (one JSON
  * header line, then raw little-endian f64 sections in header order, x

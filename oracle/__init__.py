@@ -59,6 +59,10 @@ lib.rgfo_solve.argtypes = [_vp, _vp, _d, ctypes.c_int, _vp, _vp, _vp, _vp, _vp, 
 lib.rgfo_op_uniform.argtypes = [_vp, _i64, ctypes.c_int]
 lib.rgfo_resolve_thread_count.argtypes = [ctypes.c_int]
 lib.rgfo_io_last_error.restype = ctypes.c_char_p
+lib.rgfo_diag_last_error.restype = ctypes.c_char_p
+lib.rgfo_impulse_response.argtypes = [_d, ctypes.c_int, ctypes.c_int, _i64, ctypes.c_int, _vp,
+                                      _vp, _vp, _vp]
+lib.rgfo_remark1.argtypes = [_vp, _i64, _d, ctypes.c_int, ctypes.c_int, ctypes.c_int, _vp]
 lib.rgfo_load_grid.argtypes = [ctypes.c_char_p, _i64, _i64, _vp, _vp, _vp, ctypes.POINTER(_i64)]
 lib.rgfo_save_grid.argtypes = [ctypes.c_char_p, _i64, _i64, _i64, _vp, _vp, _vp]
 lib.rgfo_load_scale.argtypes = [ctypes.c_char_p, _i64, _i64, _vp, _vp]
@@ -293,3 +297,24 @@ def save_field(path, values):
     ny, nx = np.shape(values)
     v = np.ascontiguousarray(values, dtype=np.float64)
     _io_check(lib.rgfo_save_field(str(path).encode(), nx, ny, _p(v)))
+
+
+# ---------------------------------------------------------------- diagnostics
+def impulse_response(sigma, order, k, length, calibration=0):
+    """diagnostics.cpp:69-96 -> (h, sum_h, err_h_l2, err_h_max)."""
+    h = np.empty(length)
+    o = np.empty(3)
+    if lib.rgfo_impulse_response(float(sigma), int(order), int(k), int(length), int(calibration),
+                                 _p(h), _p(o[0:]), _p(o[1:]), _p(o[2:])) != 0:
+        raise OracleError(lib.rgfo_diag_last_error().decode())
+    return h, o[0], o[1], o[2]
+
+
+def remark1(s0, sigma, order, k, calibration=0):
+    """diagnostics.cpp:102-135 -> (lhs, rhs, err_h_l2, holds)."""
+    x = np.ascontiguousarray(s0, dtype=np.float64)
+    o = np.empty(4)
+    if lib.rgfo_remark1(_p(x), x.size, float(sigma), int(order), int(k), int(calibration),
+                        _p(o)) != 0:
+        raise OracleError(lib.rgfo_diag_last_error().decode())
+    return o[0], o[1], o[2], bool(o[3])

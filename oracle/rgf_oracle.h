@@ -95,6 +95,13 @@ int rgfo_save_scale(const char* path, int64_t nx, int64_t ny, const double* rx, 
 int rgfo_load_field(const char* path, int64_t nx, int64_t ny, double* values);
 int rgfo_save_field(const char* path, int64_t nx, int64_t ny, const double* values);
 
+/* diagnostics.cpp:69-135 (rgf_oracle_diag.cpp) */
+const char* rgfo_diag_last_error(void);
+int rgfo_impulse_response(double sigma, int order, int k, int64_t length, int calibration,
+                          double* h, double* sum_h, double* err_l2, double* err_max);
+int rgfo_remark1(const double* s0, int64_t m, double sigma, int order, int k, int calibration,
+                 double* out4);
+
 #ifdef __cplusplus
 }
 #endif

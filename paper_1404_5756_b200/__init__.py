@@ -32,6 +32,7 @@ __all__ = [
     "rf3_filter_coefficients", "rf1_coefficients_table", "rf3_filter", "rf1_filter",
     "container_info", "load_grid", "save_grid", "load_scale_field", "save_scale_field",
     "load_state_field", "save_state_field", "IOError_",
+    "impulse_responses", "remark1_bound_checks", "ImpulseReports",
     "lib", "LIB_PATH",
 ]
 
@@ -81,6 +82,10 @@ lib.rgf_rf1_coefficients.argtypes = [ctypes.c_double, ctypes.c_int, _dp]
 lib.rgf_rf3_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
 lib.rgf_rf1_apply_1d.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, _vp]
 lib.rgf_rf3_cascade_variance.argtypes = [ctypes.c_double, _dp]
+lib.rgf_impulse_responses.argtypes = [_vp, _i64, ctypes.c_int, ctypes.c_int, _i64, ctypes.c_int,
+                                      _vp, _vp, _vp, _vp]
+lib.rgf_remark1_checks.argtypes = [_vp, _vp, _i64, _i64, ctypes.c_int, ctypes.c_int, ctypes.c_int,
+                                   _vp]
 lib.rgf_container_info.argtypes = [ctypes.c_char_p, ctypes.c_char_p, ctypes.POINTER(_i64),
                                    ctypes.POINTER(_i64), ctypes.POINTER(_i64),
                                    ctypes.POINTER(_i64)]
@@ -533,6 +538,54 @@ def rf1_filter(x, c: Rf1Coefficients, transpose=False):
     x = np.asarray(x, dtype=np.float64)
     return _filter_tables(x, x.shape[-1], lib.rgf_rf1_filter, (c.alpha, c.beta),
                           int(c.k_iterations), int(bool(transpose)))
+
+
+# --------------------------------------------------------------------------
+# Batched diagnostics (diagnostics.cpp:69-135)
+@dataclass
+class ImpulseReports:  # diagnostics.hpp ImpulseReport, one row per study
+    sigma: np.ndarray
+    order: FilterOrder
+    k: int
+    h: np.ndarray        # (n, length) raw responses to a Dirac at length/2
+    g: np.ndarray        # (n, length) sampled Gaussians at the same offsets
+    sum_h: np.ndarray
+    err_h_l2: np.ndarray
+    err_h_max: np.ndarray
+
+
+def impulse_responses(sigmas, order: FilterOrder, k: int, length: int,
+                      calibration: Rf3Calibration = Rf3Calibration.yvv95) -> ImpulseReports:
+    """impulse_response (diagnostics.cpp:69-96) for many sigmas at once, one
+    device thread per study."""
+    sig = np.ascontiguousarray(np.atleast_1d(sigmas), dtype=np.float64)
+    n = sig.size
+    h = np.empty((n, length))
+    o = np.empty((3, n))
+    ordv = RGF_ORDER[FilterOrder(order)]
+    _check(lib.rgf_impulse_responses(_ptr(sig), n, ordv, int(k), int(length), int(calibration),
+                                     _ptr(h), _ptr(o[0]), _ptr(o[1]), _ptr(o[2])))
+    c = length // 2
+    off = np.arange(length) - c
+    g = np.exp(-(off[None, :] ** 2) / (2 * sig[:, None] ** 2))
+    return ImpulseReports(sig, FilterOrder(order), int(k), h, g, o[0].copy(), o[1].copy(),
+                          o[2].copy())
+
+
+def remark1_bound_checks(s0, sigmas, order: FilterOrder, k: int,
+                         calibration: Rf3Calibration = Rf3Calibration.yvv95) -> dict:
+    """remark1_bound_check (diagnostics.cpp:102-135) for n inputs (n, m) with
+    one sigma each -> arrays lhs, rhs, err_h_l2, holds."""
+    x = np.ascontiguousarray(np.atleast_2d(s0), dtype=np.float64)
+    n, m = x.shape
+    sig = np.ascontiguousarray(np.broadcast_to(np.asarray(sigmas, dtype=np.float64), (n,)))
+    o = np.empty((n, 4))
+    _check(lib.rgf_remark1_checks(_ptr(x), _ptr(sig), n, m, RGF_ORDER[FilterOrder(order)], int(k),
+                                  int(calibration), _ptr(o)))
+    return {"lhs": o[:, 0], "rhs": o[:, 1], "err_h_l2": o[:, 2], "holds": o[:, 3] != 0}
+
+
+RGF_ORDER = {FilterOrder.first: 1, FilterOrder.third: 3}
 
 
 # --------------------------------------------------------------------------

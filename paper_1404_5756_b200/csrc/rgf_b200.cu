@@ -28,6 +28,7 @@
 #include "closures.cuh"
 #include "solver_kernels.cuh"
 #include "container_io.cuh"
+#include "diag_kernels.cuh"
 
 namespace {
 
@@ -792,6 +793,61 @@ void check_dims(int64_t nx, int64_t ny, int64_t nlev) {
 extern "C" {
 
 const char* rgf_last_error(void) { return g_last_error.c_str(); }
+
+// --------------------------------------------------------- diagnostics
+// diagnostics.cpp:69-96 impulse_response, batched over n studies (host arrays)
+int rgf_impulse_responses(const double* sigma, int64_t n, int order, int k, int64_t length,
+                          int calibration, double* h, double* sum_h, double* err_h_l2,
+                          double* err_h_max) {
+  return guarded([&] {
+    if (length < 4) throw InvalidArgument("impulse_response: length must be >= 4");
+    if (n < 1) throw InvalidArgument("impulse_response: no studies");
+    if (!sigma || !h || !sum_h || !err_h_l2 || !err_h_max)
+      throw InvalidArgument("impulse_response: null argument");
+    for (int64_t s = 0; s < n; ++s)
+      if (!(sigma[s] > 0)) throw InvalidArgument("impulse_response: sigma must be positive");
+    if (order != RGF_ORDER_FIRST && order != RGF_ORDER_THIRD)
+      throw InvalidArgument("covariance: order must be 1 or 3");
+    if (order == RGF_ORDER_THIRD && k != 1)
+      throw InvalidArgument("the third-order filter is single-iteration by construction");
+    if (order == RGF_ORDER_FIRST && k < 1) throw InvalidArgument("rf1_coefficients: k must be >= 1");
+    DevBuf<double> sg, dh, o3;
+    sg.upload(sigma, static_cast<size_t>(n));
+    dh.alloc(static_cast<size_t>(n * length));
+    o3.alloc(static_cast<size_t>(3 * n));
+    rgfb::k_impulse<<<grid_for(n, 64), 64>>>(sg.p, n, order, k, length, calibration, dh.p, o3.p,
+                                             o3.p + n, o3.p + 2 * n);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpy(h, dh.p, static_cast<size_t>(n * length) * 8, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(sum_h, o3.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(err_h_l2, o3.p + n, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+    CUDA_OK(cudaMemcpy(err_h_max, o3.p + 2 * n, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost));
+  });
+}
+
+// diagnostics.cpp:102-135 remark1_bound_check, batched: s0 is n x m, one
+// sigma per study; out4[s] = {lhs, rhs, err_h_l2, holds}
+int rgf_remark1_checks(const double* s0, const double* sigma, int64_t n, int64_t m, int order,
+                       int k, int calibration, double* out4) {
+  return guarded([&] {
+    if (m < 4) throw InvalidArgument("remark1_bound_check: input too short");
+    if (n < 1 || !s0 || !sigma || !out4) throw InvalidArgument("remark1_bound_check: null argument");
+    for (int64_t p = 0; p < n * m; ++p)
+      if (!std::isfinite(s0[p])) throw InvalidArgument("remark1_bound_check: input must be finite");
+    for (int64_t s = 0; s < n; ++s)
+      if (!(sigma[s] > 0)) throw InvalidArgument("remark1_bound_check: sigma must be positive");
+    if (order == RGF_ORDER_THIRD && k != 1)
+      throw InvalidArgument("the third-order filter is single-iteration by construction");
+    DevBuf<double> x, sg, scr, o;
+    x.upload(s0, static_cast<size_t>(n * m));
+    sg.upload(sigma, static_cast<size_t>(n));
+    scr.alloc(static_cast<size_t>(3 * n * m));
+    o.alloc(static_cast<size_t>(4 * n));
+    rgfb::k_remark1<<<grid_for(n, 64), 64>>>(x.p, sg.p, n, m, order, k, calibration, scr.p, o.p);
+    CUDA_OK(cudaGetLastError());
+    CUDA_OK(cudaMemcpy(out4, o.p, static_cast<size_t>(4 * n) * 8, cudaMemcpyDeviceToHost));
+  });
+}
 
 // --------------------------------------------------------- container I/O
 int rgf_container_info(const char* path, char* format, int64_t* nx, int64_t* ny,

@@ -619,3 +619,31 @@ def test_1d_entry_points_with_coefficient_tables(P):
         P.rf3_filter(np.zeros(3), P.rf3_filter_coefficients(np.ones(3)))
     with pytest.raises(P.InvalidArgument, match="sigma must be positive"):
         P.rf3_filter_coefficients(np.array([1.0, -1.0]))
+
+
+def test_batched_diagnostics_match_oracle(P):
+    """Many impulse studies and Remark-1 checks at once (diagnostics.cpp:69-135,
+    SURVEY §8f row 4), one device thread per study, against the oracle's
+    per-study restatement: responses within 1e-13 of their peak, the error
+    norms within 1e-10 relative (device exp vs glibc exp), same verdicts."""
+    sig = np.array([0.7, 1.5, 2.0, 4.0, 6.5, 10.0])
+    for order, k in ((3, 1), (1, 1), (1, 5)):
+        rep = P.impulse_responses(sig, P.FilterOrder.third if order == 3 else P.FilterOrder.first,
+                                  k, 257)
+        for i, s0 in enumerate(sig):
+            h, sh, e2, emax = O.impulse_response(s0, order, k, 257)
+            assert np.max(np.abs(rep.h[i] - h)) <= 1e-13 * np.max(np.abs(h))
+            assert rep.sum_h[i] == pytest.approx(sh, rel=1e-13)
+            assert rep.err_h_l2[i] == pytest.approx(e2, rel=1e-10)
+            assert rep.err_h_max[i] == pytest.approx(emax, rel=1e-10)
+    x = np.random.default_rng(32).standard_normal((6, 301))
+    for order, k in ((3, 1), (1, 5)):
+        r = P.remark1_bound_checks(x, sig, P.FilterOrder.third if order == 3 else P.FilterOrder.first, k)
+        for i in range(6):
+            lhs, rhs, err, holds = O.remark1(x[i], sig[i], order, k)
+            assert r["lhs"][i] == pytest.approx(lhs, rel=1e-10)
+            assert r["rhs"][i] == pytest.approx(rhs, rel=1e-10)
+            assert r["err_h_l2"][i] == pytest.approx(err, rel=1e-10)
+            assert bool(r["holds"][i]) == holds
+    with pytest.raises(P.InvalidArgument, match="length must be >= 4"):
+        P.impulse_responses([2.0], P.FilterOrder.third, 1, 3)
