@@ -66,6 +66,16 @@ int guarded(F&& f) {
   }
 }
 
+// RGF_B200_DEBUG_POISON=1: fill every new device buffer with 0xff bytes, so a
+// read of memory nobody wrote shows up deterministically
+bool debug_poison() {
+  static const bool on = [] {
+    const char* e = std::getenv("RGF_B200_DEBUG_POISON");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <typename T>
 struct DevBuf {
   T* p = nullptr;
@@ -74,8 +84,15 @@ struct DevBuf {
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
   ~DevBuf() { release(); }
+  // Buffers only grow; a growing apply-scratch buffer may still be read by
+  // kernels in flight on a non-blocking stream (e.g. the checkpoint buffer of
+  // a transposed x sweep while the y sweep re-sizes it), and cudaFree does
+  // not wait for those: drain the device first (rare: growth only).
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaDeviceSynchronize();
+      cudaFree(p);
+    }
     p = nullptr;
     n = 0;
   }
@@ -85,6 +102,7 @@ struct DevBuf {
     if (count == 0) return;
     CUDA_OK(cudaMalloc(&p, count * sizeof(T)));
     n = count;
+    if (debug_poison()) CUDA_OK(cudaMemset(p, 0xff, count * sizeof(T)));  // NaN / -1 patterns
   }
   void upload(const T* h, size_t count) {
     alloc(count);
@@ -92,6 +110,26 @@ struct DevBuf {
   }
   size_t bytes() const { return n * sizeof(T); }
 };
+
+// RGF_B200_DEBUG_SYNC=1: synchronize and check after every launch group, so
+// an asynchronous fault is reported at the launch that caused it
+// (compute-sanitizer is not available on the GPU pool)
+bool debug_sync() {
+  static const bool on = [] {
+    const char* e = std::getenv("RGF_B200_DEBUG_SYNC");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+#define RGF_DEBUG_SYNC(st, what)                                                      \
+  do {                                                                               \
+    if (debug_sync()) {                                                              \
+      const cudaError_t e2_ = cudaStreamSynchronize(st);                            \
+      if (e2_ != cudaSuccess)                                                        \
+        throw CudaError(std::string("debug sync after ") + (what) + ": " +           \
+                        cudaGetErrorString(e2_));                                    \
+    }                                                                                \
+  } while (0)
 
 int grid_for(int64_t work, int threads, int max_blocks = 148 * 16) {
   int64_t b = (work + threads - 1) / threads;
@@ -139,7 +177,9 @@ struct rgf_op {
   // streaming 3rd-RF path: bit-packed masks, closure classes and tables
   bool stream_ok = false;
   bool ckpt_ok = true;  // TMA-fed sweeps (checkpointed / single-pass) for this op's tables
-  bool xt_env = false;   // RGF_B200_XT=1 at creation: few-plane x sweeps on the transposed field
+  // few-plane x sweeps on the transposed field (lanes = rows instead of
+  // planes): default on; RGF_B200_XT=0 at creation turns it off
+  bool xt_mode = true;
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
@@ -319,11 +359,14 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.pre_scale = pre;
     a.post_scale = post;
     // few planes: the x sweep's lanes would be planes, mostly idle; run it as
-    // a y sweep (lanes = rows) on the transposed field instead. Opt-in
-    // (RGF_B200_XT=1, read per sweep): 1024^2 single level 2x faster, C3
-    // level 0 slower (one plane leaves 7 of the y CTA's 8 plane-warps idle),
-    // DESIGN §10.
-    if (op->xt_env && dir == 0 && op->ckpt_ok && nvar * nlev <= 8 && !pre && !post &&
+    // a y sweep (lanes = rows) on the transposed field instead, with the
+    // few-plane y shapes (launch_yck1 / launch_yck2). Default for <= 2 planes
+    // (RGF_B200_XT=0 at creation turns it off); DESIGN §3.9. fp64 only: the
+    // transposed sweep then has the x sweep's 16-point blocks, so results are
+    // bit-identical to the direct x kernels (host pipeline chunks and level
+    // shards of any size agree bit for bit); fp32 x blocks are 32 points.
+    if (op->xt_mode && sizeof(T) == 8 && dir == 0 && op->ckpt_ok && nvar * nlev <= 2 && !pre &&
+        !post &&
         rgfb::tma_supported(in, out, pitch)) {
       if (!op->xt_ok) build_xt(op, st);
       // transposed rows (length ny) padded to a 16 B pitch for the TMA maps
@@ -334,6 +377,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
       T* ti = reinterpret_cast<T*>(op->xt_in.p);
       T* to = reinterpret_cast<T*>(op->xt_out.p);
       transpose_planes<T>(in, ti, op->nx, op->ny, pitch, pt, planes, st);
+      RGF_DEBUG_SYNC(st, "xt transpose in");
       rgfb::StreamArgs b = a;
       b.dir = 1;
       b.nx = op->ny;
@@ -350,8 +394,10 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
       op->ckpt.alloc(static_cast<size_t>(std::max<int64_t>(1, rgfb::ckpt_doubles<T>(b))));
       op->launches +=
           static_cast<unsigned long long>(rgfb::launch_ckpt_sweep<T>(ti, to, b, op->ckpt.p, st));
+      RGF_DEBUG_SYNC(st, "xt ckpt sweep");
       CUDA_OK(cudaGetLastError());
       transpose_planes<T>(to, out, op->ny, op->nx, pt, pitch, planes, st);
+      RGF_DEBUG_SYNC(st, "xt transpose out");
       op->launches += 2;
       return;
     }
@@ -360,6 +406,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
       op->launches +=
           static_cast<unsigned long long>(rgfb::launch_ckpt_sweep<T>(in, out, a, op->ckpt.p, st));
       CUDA_OK(cudaGetLastError());
+      RGF_DEBUG_SYNC(st, dir == 0 ? "x ckpt sweep" : "y ckpt sweep");
       return;
     }
     if (pitch != op->nx) throw std::runtime_error("sweep: pitched field on a dense-only path");
@@ -399,6 +446,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     a.post_scale = post;
     op->launches += static_cast<unsigned long long>(rgfb::launch_rf1_sweep<T>(in, out, a, st));
     CUDA_OK(cudaGetLastError());
+    RGF_DEBUG_SYNC(st, "rf1 sweep");
     return;
   }
 
@@ -1297,7 +1345,7 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         CUDA_OK(cudaDeviceSynchronize());
         op->stream_ok = true;
         const char* xte = std::getenv("RGF_B200_XT");
-        op->xt_env = xte && xte[0] == '1';
+        op->xt_mode = !(xte && xte[0] == '0');
         if (op->ckpt_ok) {
           for (int dir = 0; dir < 2; ++dir) {
             const int64_t tot = g->nlev * (dir == 0 ? g->ny : g->nx) * op->words[dir];

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
         const int u = q * EPC + e;
         if ((starts >> u) & 1u) st.reset();
         double w = v[e];
-        if constexpr (TR && VAR) w *= __ldg(PRE + k0 + u);
+        if constexpr (TR && VAR) w *= __ldg(PRE + (k0 + u < n ? k0 + u : n - 1));
         if constexpr (TR && IDC) w *= id[u];
         st.step(cf[u], w);
       }
@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
           const int u = q * EPC + e;
           if ((starts >> u) & 1u) st.reset();
           double w = v[e];
-          if constexpr (TR && VAR) w *= __ldg(PRE + k0 + u);
+          if constexpr (TR && VAR) w *= __ldg(PRE + (k0 + u < n ? k0 + u : n - 1));
           if constexpr (TR && IDC) w *= id[u];
           st.step(cf[u], w);
         }
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(32 * R * NWR, 1)
           const int u = t * U + q * EPC + e;
           reset_if(sa, (starts >> u) & 1u);
           double w = v[e];
-          if constexpr (TR && PRE) w *= __ldg(PREp + kb + u);
+          if constexpr (TR && PRE) w *= __ldg(PREp + (kb + u < n ? kb + u : n - 1));
           if constexpr (TR && IDC) w *= id[u];
           pv[u] = sa.step(cfu(u), w);
         }
@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(32 * R * NWR, 1)
           }
           double ov = sd.step(c, c.b * pv[u]);
           if constexpr (!TR && IDC) ov *= id[u];
-          if constexpr (POST) ov *= __ldg(POSTp + kb + u);
+          if constexpr (POST) ov *= __ldg(POSTp + (kb + u < n ? kb + u : n - 1));
           o[e] = ((sb >> u) & 1u) ? ov : 0.0;
         }
         if constexpr (sizeof(T) == 8) {
@@ -915,7 +915,7 @@ __global__ void __launch_bounds__(32 * R * NWR, 1)
           const int u = q * EPC + e;
           reset_if(sa, (starts >> u) & 1u);
           double w = v[e];
-          if constexpr (TR && PRE) w *= __ldg(PREp + kb + u);
+          if constexpr (TR && PRE) w *= __ldg(PREp + (kb + u < n ? kb + u : n - 1));
           if constexpr (TR && IDC) w *= id[u];
           pv[u] = sa.step(cfu(u), w);
         }
@@ -949,7 +949,7 @@ __global__ void __launch_bounds__(32 * R * NWR, 1)
           }
           double ov = sd.step(c, c.b * pv[u]);
           if constexpr (!TR && IDC) ov *= id[u];
-          if constexpr (POST) ov *= __ldg(POSTp + kb + u);
+          if constexpr (POST) ov *= __ldg(POSTp + (kb + u < n ? kb + u : n - 1));
           o[e] = ((sb >> u) & 1u) ? ov : 0.0;
         }
         if constexpr (sizeof(T) == 8) {
@@ -1039,7 +1039,9 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
       const uint64_t pol_stream = l2_evict_first(), pol_keep = l2_evict_last();
       tma_prefetch_desc(&tm_field);
       tma_prefetch_desc(&tm_coef);
-      const uint32_t total = static_cast<uint32_t>(L::field + L::coef + (IDC ? L::idc : 0));
+      // the field box holds box_planes planes (few-plane operators: no zero fill)
+      const uint32_t total = static_cast<uint32_t>(
+          size_t(a.box_planes) * U * 32 * sizeof(T) + L::coef + (IDC ? L::idc : 0));
       for (int64_t i = 0; i < nst; ++i) {
         const int s = static_cast<int>(i % S);
         const int64_t m = i / S;
@@ -1085,7 +1087,7 @@ __global__ void __launch_bounds__(32 * (NW + 1), 1)
     for (int r = 0; r < U; ++r) {
       if ((starts >> r) & 1u) st.reset();
       double w = static_cast<double>(fld[r * 32]);
-      if constexpr (TR && VAR) w *= __ldg(PREp + (lo + r) * nx);
+      if constexpr (TR && VAR) w *= __ldg(PREp + (lo + r < ny ? lo + r : ny - 1) * nx);
       if constexpr (TR && IDC) w *= id[r * 32];
       st.step(coef_soa<U>(cs, r, lane), w);
     }
@@ -1116,7 +1118,8 @@ struct YC2 {
 // planes (independent chains interleaved: ILP, and one coefficient load
 // serves PPW chains); results go straight to global memory (coalesced
 // 32-column rows).
-template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S, int LG>
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S, int LG,
+          int PD>
 __global__ void __launch_bounds__(32 * NW, NW <= 8 ? 2 : 1)
     k_yck2(T* __restrict__ out, StreamArgs a, const double* __restrict__ ck,
            const __grid_constant__ CUtensorMap tm_field, const __grid_constant__ CUtensorMap tm_coef,
@@ -1148,7 +1151,8 @@ __global__ void __launch_bounds__(32 * NW, NW <= 8 ? 2 : 1)
 
   // no producer warp: thread 0 issues block loads; a buffer is refilled once
   // every warp has finished the block it held (empty barrier)
-  const uint32_t total = static_cast<uint32_t>(L::field + L::coef + (IDC ? L::idc : 0));
+  const uint32_t total = static_cast<uint32_t>(size_t(a.box_planes) * X * 32 * sizeof(T) +
+                                               L::coef + (IDC ? L::idc : 0));
   auto load_block = [&](int64_t bi) {
     const int s = static_cast<int>(bi % S);
     const int lo = static_cast<int>((NB - 1 - bi) * X);
@@ -1209,9 +1213,13 @@ __global__ void __launch_bounds__(32 * NW, NW <= 8 ? 2 : 1)
     return load_meta<X>(ck + ((pp[c] * NB + b) * 3) * nx + ix, b > 0 && act[c], nx, W[c], nx,
                         b * X, a.words);
   };
-  BlockMeta next[PPW];
+  // per-block metadata PD blocks ahead (PD > 1 for the few-plane shape, where
+  // no other warp hides the load latency): ring[c][j] = block NB-1-(bi+j)
+  BlockMeta ring[PPW][PD];
 #pragma unroll
-  for (int c = 0; c < PPW; ++c) next[c] = meta(c, NB - 1);
+  for (int c = 0; c < PPW; ++c)
+#pragma unroll
+    for (int j = 0; j < PD; ++j) ring[c][j] = meta(c, NB - 1 - j >= 0 ? NB - 1 - j : 0);
 
   for (int64_t bi = 0; bi < NB; ++bi) {
     const int s = static_cast<int>(bi % S);
@@ -1227,8 +1235,10 @@ __global__ void __launch_bounds__(32 * NW, NW <= 8 ? 2 : 1)
     Closure mpre[PPW];
 #pragma unroll
     for (int c = 0; c < PPW; ++c) {
-      const BlockMeta cur = next[c];
-      if (b > 0) next[c] = meta(c, b - 1);  // consumed one block from now
+      const BlockMeta cur = ring[c][0];
+#pragma unroll
+      for (int j = 0; j + 1 < PD; ++j) ring[c][j] = ring[c][j + 1];
+      ring[c][PD - 1] = meta(c, b - PD >= 0 ? b - PD : 0);  // consumed PD blocks from now
       r1[c] = cur.r1;
       r2[c] = cur.r2;
       r3[c] = cur.r3;
@@ -1262,7 +1272,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 8 ? 2 : 1)
       for (int c = 0; c < PPW; ++c) {
         reset_if(sa[c], (starts[c] >> u) & 1u);
         double w = static_cast<double>(fld[(c * X + u) * 32]);
-        if constexpr (TR && PRE) w *= __ldg(PREp[c] + (kb + u) * nx);
+        if constexpr (TR && PRE) w *= __ldg(PREp[c] + (kb + u < ny ? kb + u : ny - 1) * nx);
         if constexpr (TR && IDC) w *= idu;
         pv[c][u] = sa[c].step(cu, w);
       }
@@ -1294,7 +1304,7 @@ __global__ void __launch_bounds__(32 * NW, NW <= 8 ? 2 : 1)
         }
         double o = sd[c].step(cu, cu.b * pv[c][u]);
         if constexpr (!TR && IDC) o *= idu;
-        if constexpr (POST) o *= __ldg(POSTp[c] + (kb + u) * nx);
+        if constexpr (POST) o *= __ldg(POSTp[c] + (kb + u < ny ? kb + u : ny - 1) * nx);
         st_cs_if(dp[c], ((sb[c] >> u) & 1u) ? o : 0.0, act[c] && u < rvalid);
         dp[c] -= a.pitch;
       }
@@ -1514,9 +1524,8 @@ inline CUtensorMap coef_soa_map(const StreamArgs& a, uint32_t rows) {
   return make_tmap(a.c3s, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 4, d, s, b, CU_TENSOR_MAP_SWIZZLE_NONE);
 }
 
-template <typename T, bool TR, bool IDC, bool VAR>
-void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) {
-  constexpr int NW = kYc1NW, U = kYc1U, S = kYc1S;
+template <typename T, bool TR, bool IDC, bool VAR, int NW, int U, int S>
+void launch_yck1_shape(const T* in, const StreamArgs& a0, double* ck, cudaStream_t st) {
   using L = YC1<T, NW, U>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
@@ -1525,11 +1534,13 @@ void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  const int64_t planes = a.nvar * a.nlev;
+  const int64_t planes = a0.nvar * a0.nlev;
+  StreamArgs a = a0;
+  a.box_planes = static_cast<int>(planes < NW ? planes : NW);
   const uint64_t sz = sizeof(T);
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
   const uint64_t fs[2] = {uint64_t(a.pitch) * sz, uint64_t(a.pitch * a.ny) * sz};
-  const uint32_t fb[3] = {32, uint32_t(U), uint32_t(NW)};
+  const uint32_t fb[3] = {32, uint32_t(U), uint32_t(a.box_planes)};
   const CUtensorMap tf = make_tmap(in, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tc = coef_soa_map(a, U);
   const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
@@ -1542,23 +1553,37 @@ void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) 
   k_yck1<T, TR, IDC, VAR, NW, U, S><<<blocks, 32 * (NW + 1), smem, st>>>(a, ck, tf, tc, ti);
 }
 
-template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S, int LG = 1>
-void launch_yck2_shape(const T* in, T* out, const StreamArgs& a, const double* ck,
+// few planes (a single level: the reference's own 2-D operator, the CG
+// solver): 4-plane CTAs with an 8-deep stage ring, so the serial walk down a
+// column is not latency-bound on the box round trips
+template <typename T, bool TR, bool IDC, bool VAR>
+void launch_yck1(const T* in, const StreamArgs& a, double* ck, cudaStream_t st) {
+  if (a.nvar * a.nlev <= 4)
+    launch_yck1_shape<T, TR, IDC, VAR, 4, kYc1U, 12>(in, a, ck, st);
+  else
+    launch_yck1_shape<T, TR, IDC, VAR, kYc1NW, kYc1U, kYc1S>(in, a, ck, st);
+}
+
+template <typename T, bool TR, bool IDC, bool PRE, bool POST, int NW, int PPW, int S, int LG = 1,
+          int PD = 1>
+void launch_yck2_shape(const T* in, T* out, const StreamArgs& a0, const double* ck,
                        cudaStream_t st) {
   constexpr int NPL = NW * PPW;
   using L = YC2<T, NPL>;
   const size_t smem = S * L::bytes + 2 * S * sizeof(uint64_t) + 1024;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S, LG>,
+    cudaFuncSetAttribute(k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S, LG, PD>,
                          cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     attr = true;
   }
-  const int64_t planes = a.nvar * a.nlev;
+  const int64_t planes = a0.nvar * a0.nlev;
+  StreamArgs a = a0;
+  a.box_planes = static_cast<int>(planes < NPL ? planes : NPL);
   const uint64_t sz = sizeof(T);
   const uint64_t fd[3] = {uint64_t(a.nx), uint64_t(a.ny), uint64_t(planes)};
   const uint64_t fs[2] = {uint64_t(a.pitch) * sz, uint64_t(a.pitch * a.ny) * sz};
-  const uint32_t fb[3] = {32, uint32_t(L::X), uint32_t(NPL)};
+  const uint32_t fb[3] = {32, uint32_t(L::X), uint32_t(a.box_planes)};
   const CUtensorMap tf = make_tmap(in, tma_dtype<T>(), 3, fd, fs, fb, CU_TENSOR_MAP_SWIZZLE_NONE);
   const CUtensorMap tc = coef_soa_map(a, L::X);
   const uint64_t id[2] = {uint64_t(a.nx), uint64_t(a.ny)};
@@ -1568,12 +1593,16 @@ void launch_yck2_shape(const T* in, T* out, const StreamArgs& a, const double* c
                                          CU_TENSOR_MAP_SWIZZLE_NONE)
                              : tc;
   const int64_t blocks = ((a.nx + 31) / 32) * ((planes + NPL - 1) / NPL);
-  k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S, LG><<<blocks, 32 * NW, smem, st>>>(out, a, ck, tf,
+  k_yck2<T, TR, IDC, PRE, POST, NW, PPW, S, LG, PD><<<blocks, 32 * NW, smem, st>>>(out, a, ck, tf,
                                                                               tc, ti);
 }
 
 template <typename T, bool TR, bool IDC, bool PRE, bool POST>
 void launch_yck2(const T* in, T* out, const StreamArgs& a, const double* ck, cudaStream_t st) {
+  if (a.nvar * a.nlev <= 2) {  // few planes: 2-plane CTAs, 6 buffers in flight
+    launch_yck2_shape<T, TR, IDC, PRE, POST, 2, 1, 6, 1, 4>(in, out, a, ck, st);
+    return;
+  }
   launch_yck2_shape<T, TR, IDC, PRE, POST, C2Shape<T>::yNW, C2Shape<T>::yPPW, C2Shape<T>::yS,
                     C2Shape<T>::yLG>(in, out, a, ck, st);
 }

@@ -70,6 +70,7 @@ struct StreamArgs {
   double4* entry;           // [var][nsegs] anti-causal entry states
   const double* pre_scale;  // optional (nlev*nh) input multiplier (variance)
   const double* post_scale; // optional (nlev*nh) output multiplier
+  int box_planes;           // planes per TMA field box of the y kernels (<= the shape's)
 };
 
 __device__ __forceinline__ uint64_t ldw(const uint64_t* w, int64_t i) {

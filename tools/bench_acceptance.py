@@ -25,9 +25,10 @@ rng = np.random.default_rng(1)
 f = rng.standard_normal((1, 1, n, n))
 out = {"case": "1024x1024, sigma=2 uniform, all sea, unit_dc, x+y (acceptance.cpp:268-300)",
        "reference_published_1thread_Mpts": {"3rd-RF": 32.1, "1st-RF K=5": 15.1}}
-for name, order, k in (("3rd-RF", 3, 1), ("1st-RF K=5", 1, 5)):
+quick = "--quick" in sys.argv  # GPU only, 3rd-RF (profiling runs)
+for name, order, k in (("3rd-RF", 3, 1),) + ((("1st-RF K=5", 1, 5),) if not quick else ()):
     row = {}
-    for threads in (1, os.cpu_count() or 1):
+    for threads in (() if quick else (1, os.cpu_count() or 1)):
         op = O.OracleOp(n, n, one, one, mask, one * 2.0, one * 2.0, order=order, k_iterations=k,
                         threads=threads)
         ts = []
@@ -54,10 +55,24 @@ for name, order, k in (("3rd-RF", 3, 1), ("1st-RF K=5", 1, 5)):
         ts.append(a.elapsed_time(b) * 1e-3)
     row["b200_Mpts"] = n * n / statistics.median(ts) / 1e6
     row["b200_ms"] = statistics.median(ts) * 1e3
-    want = O.OracleOp(n, n, one, one, mask, one * 2.0, one * 2.0, order=order, k_iterations=k,
-                      threads=os.cpu_count() or 1).apply(O.GYGX, f)
-    got = y.cpu().numpy()
-    row["rel_max_err_vs_oracle"] = float(np.max(np.abs(got - want)) / np.max(np.abs(want)))
+    if not quick:
+        want = O.OracleOp(n, n, one, one, mask, one * 2.0, one * 2.0, order=order, k_iterations=k,
+                          threads=os.cpu_count() or 1).apply(O.GYGX, f)
+        got = y.cpu().numpy()
+        row["rel_max_err_vs_oracle"] = float(np.max(np.abs(got - want)) / np.max(np.abs(want)))
+    for sname, kind in (("x", P.GX), ("y", P.GY)):
+        ts2 = []
+        for _ in range(11):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            gop.apply(kind, x, y)
+            b.record()
+            torch.cuda.synchronize()
+            ts2.append(a.elapsed_time(b))
+        row[f"b200_{sname}_sweep_ms"] = statistics.median(ts2)
+    if quick:
+        out[name] = row
+        continue
     out[name] = row
 out["host_threads"] = os.cpu_count()
 print(json.dumps(out))
