@@ -24,6 +24,7 @@
 #include "sweep_stream.cuh"
 #include "sweep_tma.cuh"
 #include "sweep_ckpt.cuh"
+#include "sweep_few.cuh"
 #include "rf1_stream.cuh"
 #include "closures.cuh"
 #include "solver_kernels.cuh"
@@ -197,6 +198,12 @@ struct rgf_op {
   DevBuf<double> xt_c3s, xt_idc, xt_clos;
   DevBuf<uint64_t> xt_bitsT;
   DevBuf<char> xt_in, xt_out;
+  // single-level operators: chunked sweeps (sweep_few.cuh), tables per frame
+  // (0: x lines through the transposed field, 1: y lines) and part
+  bool few_mode = true;  // RGF_B200_FEW=0 at creation turns it off
+  bool few_built[2][2] = {{false, false}, {false, false}};
+  DevBuf<double> few_tab[2][2], few_chk[2][2], few_cta[2][2], few_scr;
+  int few_cs[2] = {0, 0};  // CTAs per column tile, per frame
   DevBuf<double4> entry;  // [var][segments] anti-causal entry states (apply scratch)
   int nclass = 0;
   // host-apply pipeline: H2D / compute / D2H streams, per-slot chunk buffers
@@ -318,6 +325,93 @@ void build_xt(rgf_op* op, cudaStream_t st) {
   op->xt_ok = true;
 }
 
+// Frame arguments of the chunked few-plane sweep: frame 1 = y lines of the
+// field, frame 0 = x lines as columns of the transposed field (xt tables).
+rgfb::FewArgs few_args(const rgf_op* op, int frame, int part) {
+  rgfb::FewArgs f{};
+  if (frame == 1) {
+    f.nx = op->nx;
+    f.ny = op->ny;
+    f.bits = op->bits[1].p;
+    f.words = static_cast<int>(op->words[1]);
+    f.c3 = op->dy_.c3.p;
+    f.c3s = op->dy_.c3s.p;
+    f.idc = op->unit_dc ? op->dy_.idc.p : nullptr;
+    f.idc_pitch = op->nx;
+    f.clos = op->clos.p;
+  } else {
+    f.nx = op->ny;
+    f.ny = op->nx;
+    f.bits = op->bits[0].p;
+    f.words = static_cast<int>(op->words[0]);
+    f.c3 = op->xt_c3.p;
+    f.c3s = op->xt_c3s.p;
+    f.idc = op->unit_dc ? op->xt_idc.p : nullptr;
+    f.idc_pitch = (op->ny + 1) / 2 * 2;
+    f.clos = op->xt_clos.p;
+  }
+  f.nh = op->nx * op->ny;
+  f.part = part;
+  f.ghost = op->ghost_d.p;
+  f.cls = op->cls_d.p;
+  // enough CTAs to cover the SMs: CS CTAs (a cluster, <= 8) per column tile
+  if (!op->few_cs[frame]) {
+    const int64_t tiles = (f.nx + 31) / 32;
+    int cs = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(8, 148 / tiles)));
+    while (cs > 1 && int64_t(cs) * rgfb::few::NW * 4 > f.ny) --cs;  // >= 4 rows per chunk
+    const_cast<rgf_op*>(op)->few_cs[frame] = cs;
+  }
+  f.CS = op->few_cs[frame];
+  f.R = static_cast<int>((f.ny + int64_t(f.CS) * rgfb::few::NW - 1) / (int64_t(f.CS) * rgfb::few::NW));
+  f.tab = op->few_tab[frame][part].p;
+  f.chk = op->few_chk[frame][part].p;
+  f.chk_cta = op->few_cta[frame][part].p;
+  return f;
+}
+
+// Few-plane (single-level operator) sweep in one frame: tables on first use.
+template <typename T>
+void few_sweep(rgf_op* op, int frame, bool transpose, const T* in, T* out, int64_t pitch,
+               int64_t nvar, int64_t lev0, int64_t nlev, const double* pre, const double* post,
+               cudaStream_t st) {
+  const int part = transpose ? 1 : 0;
+  if (!op->few_built[frame][part]) {
+    rgfb::FewArgs f = few_args(op, frame, part);
+    f.nlev = op->nlev;
+    op->few_tab[frame][part].alloc(static_cast<size_t>(op->nlev * f.ny * 6 * f.nx));
+    op->few_chk[frame][part].alloc(
+        static_cast<size_t>(op->nlev * f.CS * rgfb::few::NW * rgfb::few::CHKW * f.nx));
+    op->few_cta[frame][part].alloc(static_cast<size_t>(op->nlev * f.CS * 18 * f.nx));
+    f.tab = op->few_tab[frame][part].p;
+    f.chk = op->few_chk[frame][part].p;
+    f.chk_cta = op->few_cta[frame][part].p;
+    const int64_t work = op->nlev * f.nx * f.CS * rgfb::few::NW;
+    if (transpose)
+      rgfb::k_yfew_tables<true><<<grid_for(work, 128), 128, 0, st>>>(
+          f, op->few_tab[frame][part].p, op->few_chk[frame][part].p);
+    else
+      rgfb::k_yfew_tables<false><<<grid_for(work, 128), 128, 0, st>>>(
+          f, op->few_tab[frame][part].p, op->few_chk[frame][part].p);
+    rgfb::k_yfew_cta<<<grid_for(op->nlev * f.nx * f.CS, 128), 128, 0, st>>>(
+        f, op->few_chk[frame][part].p, op->few_cta[frame][part].p);
+    CUDA_OK(cudaGetLastError());
+    op->few_built[frame][part] = true;
+  }
+  rgfb::FewArgs f = few_args(op, frame, part);
+  f.pitch = pitch;
+  f.planes = nvar * nlev;
+  f.nlev = nlev;
+  f.lev0 = lev0;
+  f.pre_scale = pre;
+  f.post_scale = post;
+  op->few_scr.alloc(static_cast<size_t>(f.planes * f.ny * f.nx));
+  rgfb::launch_yfew<T>(in, out, op->few_scr.p, f, transpose, f.idc != nullptr, pre != nullptr,
+                       post != nullptr, st);
+  CUDA_OK(cudaGetLastError());
+  op->launches += 1;
+  RGF_DEBUG_SYNC(st, "few-plane sweep");
+}
+
 template <typename T>
 void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nvar,
            int64_t lev0, int64_t nlev, const double* pre, const double* post, cudaStream_t st,
@@ -365,6 +459,28 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
     // transposed sweep then has the x sweep's 16-point blocks, so results are
     // bit-identical to the direct x kernels (host pipeline chunks and level
     // shards of any size agree bit for bit); fp32 x blocks are 32 points.
+    // single-level operators (the reference's own 2-D operator): chunked
+    // sweeps, x lines through the transposed field
+    if (op->few_mode && op->nlev == 1 && op->ckpt_ok) {
+      if (dir == 1) {
+        few_sweep<T>(op, 1, transpose, in, out, pitch, nvar, lev0, nlev, pre, post, st);
+        return;
+      }
+      if (!op->xt_ok) build_xt(op, st);
+      const int64_t q = 16 / static_cast<int64_t>(sizeof(T));
+      const int64_t pt = (op->ny + q - 1) / q * q, planes = nvar * nlev;
+      op->xt_in.alloc(static_cast<size_t>(planes * op->nx * pt) * sizeof(T));
+      op->xt_out.alloc(static_cast<size_t>(planes * op->nx * pt) * sizeof(T));
+      T* ti = reinterpret_cast<T*>(op->xt_in.p);
+      T* to = reinterpret_cast<T*>(op->xt_out.p);
+      transpose_planes<T>(in, ti, op->nx, op->ny, pitch, pt, planes, st);
+      // the variance multiplies (pre/post) are [lev][iy][ix]: x sweeps never
+      // carry them (V: post on y, V^T: pre on y)
+      few_sweep<T>(op, 0, transpose, ti, to, pt, nvar, lev0, nlev, nullptr, nullptr, st);
+      transpose_planes<T>(to, out, op->ny, op->nx, pt, pitch, planes, st);
+      op->launches += 2;
+      return;
+    }
     if (op->xt_mode && sizeof(T) == 8 && dir == 0 && op->ckpt_ok && nvar * nlev <= 2 && !pre &&
         !post &&
         rgfb::tma_supported(in, out, pitch)) {
@@ -1344,6 +1460,7 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
         CUDA_OK(cudaDeviceSynchronize());
         op->stream_ok = true;
+        if (const char* fe = std::getenv("RGF_B200_FEW")) op->few_mode = fe[0] != '0';
         const char* xte = std::getenv("RGF_B200_XT");
         op->xt_mode = !(xte && xte[0] == '0');
         if (op->ckpt_ok) {

@@ -647,3 +647,27 @@ def test_batched_diagnostics_match_oracle(P):
             assert bool(r["holds"][i]) == holds
     with pytest.raises(P.InvalidArgument, match="length must be >= 4"):
         P.impulse_responses([2.0], P.FilterOrder.third, 1, 3)
+
+
+@pytest.mark.parametrize("nx,ny,sea,dt,nvar", [(96, 64, 0.8, "f64", 1), (57, 43, 0.7, "f64", 2),
+                                               (300, 5, 0.9, "f64", 1), (7, 300, 0.9, "f32", 1),
+                                               (128, 1000, 1.0, "f64", 1), (600, 217, 0.85, "f32", 3)])
+def test_single_level_chunked_sweeps(P, nx, ny, sea, dt, nvar):
+    """Single-level operators (the reference's 2-D API) run the chunked sweep
+    (sweep_few.cuh: 16 row chunks per 32-column tile, carries folded in
+    shared memory; x lines through the transposed field): every kind with
+    variance against the oracle, including lines shorter than the chunk
+    count, all-sea lines crossing every chunk, odd sizes and fp32."""
+    g, rx, ry = random_case(1200 + nx + ny, nx=nx, ny=ny, nlev=1, sea=sea, smax=9.5)
+    var = np.random.default_rng(29).uniform(0.5, 2.0, (1, ny, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, variance=var)
+    f = np.random.default_rng(30).standard_normal((nvar, 1, ny, nx))
+    tol = TOL64
+    if dt == "f32":
+        f = f.astype(np.float32)
+        tol = TOL32
+    for name in KINDS:
+        got = gpu.apply(getattr(P, name), f)
+        want = cpu.apply(getattr(O, name), f.astype(np.float64))
+        assert relmax(got, want) <= tol, (name, relmax(got, want))
+        assert np.all(got[:, ~g["mask"]] == 0.0), name
