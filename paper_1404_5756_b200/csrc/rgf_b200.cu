@@ -26,6 +26,7 @@
 #include "sweep_ckpt.cuh"
 #include "sweep_few.cuh"
 #include "rf1_stream.cuh"
+#include "rf1_line.cuh"
 #include "closures.cuh"
 #include "solver_kernels.cuh"
 #include "container_io.cuh"
@@ -148,6 +149,7 @@ struct DirData {
   DevBuf<double> idc;
   DevBuf<int64_t> seg_off;  // nlev*lines + 1
   std::vector<int64_t> seg_off_h;  // host copy (1st-RF level-chunk segment ranges)
+  int segcap = 0;                   // most segments on one line (line-resident 1st-RF)
   DevBuf<int2> segs;
   DevBuf<int32_t> seg_line;  // per segment: lev*lines + line
   DevBuf<int64_t> close_order;  // segments sorted by (line, end, level)
@@ -182,6 +184,7 @@ struct rgf_op {
   // planes): default on; RGF_B200_XT=0 at creation turns it off
   bool xt_mode = true;
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
+  bool rf1_line = true;  // line-resident 1st-RF sweeps (RGF_B200_RF1LINE=0 at creation: streaming)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
   DevBuf<double> ckpt;  // per-block causal checkpoints (apply scratch)
@@ -554,6 +557,34 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
       a.seg_end = d.seg_off_h[static_cast<size_t>((lev0 + nlev) * nl)];
     }
     a.zone = d.zone[transpose ? 1 : 0].p;
+    if (op->rf1_line) {  // all K iterations with the line resident: one field pass
+      rgfb::Rf1LineArgs b{};
+      b.dir = dir;
+      b.transpose = transpose;
+      b.k = op->k;
+      b.nx = op->nx;
+      b.ny = op->ny;
+      b.nlev = nlev;
+      b.nvar = nvar;
+      b.lev0 = lev0;
+      b.c1 = d.c1.p;
+      b.bits = op->bits[dir].p;
+      b.words = op->words[dir];
+      b.seg_off = d.seg_off.p;
+      b.segs = d.segs.p;
+      b.nsegs = d.nsegs;
+      b.zone = a.zone;
+      b.ghost = op->ghost_d.p;
+      b.pre_scale = pre;
+      b.post_scale = post;
+      b.segcap = std::max(1, d.segcap);
+      if (rgfb::launch_rf1_line<T>(in, out, b, st)) {
+        op->launches += 1;
+        CUDA_OK(cudaGetLastError());
+        RGF_DEBUG_SYNC(st, "rf1 line sweep");
+        return;
+      }
+    }
     op->rf1_hist.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs * 2 * op->k)));
     a.hist = op->rf1_hist.p;
     op->rf1_ent.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs)));
@@ -1521,6 +1552,14 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         }
         CUDA_OK(cudaDeviceSynchronize());
         op->rf1_ok = true;
+        if (const char* le = std::getenv("RGF_B200_RF1LINE")) op->rf1_line = le[0] != '0';
+        for (int dir = 0; dir < 2; ++dir) {
+          DirData& d = dir == 0 ? op->dx_ : op->dy_;
+          int64_t cap = 0;
+          for (size_t i = 0; i + 1 < d.seg_off_h.size(); ++i)
+            cap = std::max(cap, d.seg_off_h[i + 1] - d.seg_off_h[i]);
+          d.segcap = static_cast<int>(cap);
+        }
       }
     }
     if (opt->variance) {
