@@ -49,6 +49,7 @@ struct Rf1LineArgs {
   int64_t nsegs;            // zone stride
   const double* zone;       // [2K][nsegs]: hL[0..K), cR[0..K)
   const int* ghost;         // per level
+  const uint8_t* same;      // per level: mask and ghost width equal the previous level's
   const double* pre_scale;  // adjoint: input multiplier (nlev*nh) or null
   const double* post_scale; // output multiplier or null
   int segcap;               // max segments per line of this direction
@@ -353,6 +354,391 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_line(const T* __restrict__ in,
   }
 }
 
+// ------------------------------------------------------------ row kernel
+// Register-resident form for lines that are rows of the field (x sweeps, and y
+// sweeps on a transposed field): thread t keeps its V points AND their links in
+// registers for all 2K passes, so a pass touches shared memory only where a
+// value changes hands: a land slot next to a segment is re-read (its entry
+// was placed by the boundary phase) and a segment's exit point is published.
+// The chunk aggregates are scanned by every warp with shuffles (no idle
+// warps) and the warp totals folded through shared memory.
+struct Rf1RowArgs {
+  int transpose, k;
+  int n, nl;                // points per line, lines per level
+  int64_t nlev, nvar, lev0;
+  const double2* c1;        // (alpha, beta): point (line, i) at c1[line*csl + i*csp]
+  int64_t csp, csl;
+  const uint64_t* bits;     // [(lev*nl + line)*words + w]
+  int64_t words;
+  const int64_t* seg_off;
+  const int2* segs;
+  int64_t nsegs;
+  const double* zone;
+  const int* ghost;
+  const uint8_t* same;      // per level: mask and ghost width equal the previous level's
+  const double* pre_scale;  // [lev][line][i] (dense rows) or null
+  const double* post_scale;
+  int segcap;
+  int planes_per_cta;
+};
+
+// predicated shared-memory exchange on a precomputed 32-bit shared address (the
+// compiler otherwise rebuilds the base address for every predicated access)
+__device__ __forceinline__ void rf1l_lds_if(double& v, uint32_t addr, uint32_t on) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p ld.shared.f64 %0, [%1];\n}\n"
+               : "+d"(v)
+               : "r"(addr), "r"(on)
+               : "memory");
+}
+__device__ __forceinline__ void rf1l_sts_if(uint32_t addr, double v, uint32_t on) {
+  asm volatile("{\n .reg .pred p;\n setp.ne.u32 p, %2, 0;\n @p st.shared.f64 [%0], %1;\n}\n" ::"r"(addr),
+               "d"(v), "r"(on)
+               : "memory");
+}
+
+template <int NT, int V>
+struct Rf1RowSmem {
+  static constexpr int CAP = NT * V;
+  static constexpr int MWW = CAP / 64 + 2;
+  static constexpr int NW = NT / 32;
+  static size_t bytes(int K, int segcap) {
+    size_t b = size_t(2) * CAP * sizeof(double);        // exchange line + input staging
+    b += size_t(2) * NW * sizeof(double);               // warp totals
+    b += size_t(4) * K * segcap * sizeof(double);       // zone cache + histories
+    b += size_t(segcap) * sizeof(int2);
+    b += size_t(MWW + 1) * sizeof(uint64_t);            // mask words, mbarrier
+    return b;
+  }
+};
+
+// same[lev] = 1 when level lev has the mask of level lev-1 (caller presets 1)
+__global__ void k_mask_same(const uint8_t* __restrict__ mask, int64_t nh, int64_t nlev,
+                            uint8_t* __restrict__ same) {
+  const int64_t total = nh * (nlev - 1);
+  for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < total;
+       q += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t lev = 1 + q / nh;
+    if ((mask[q + nh] != 0) != (mask[q] != 0)) same[lev] = 0;
+  }
+}
+
+__device__ __forceinline__ void rf1l_cp_async(void* dst, const void* src, int bytes) {
+  if (bytes == 8)
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+  else
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+
+template <typename T, bool TR, int NT, int V, int MINB>
+__global__ void __launch_bounds__(NT, MINB) k_rf1_row(const T* __restrict__ in, T* __restrict__ out,
+                                                      Rf1RowArgs a) {
+  using L = Rf1RowSmem<NT, V>;
+  constexpr int CAP = L::CAP, MWW = L::MWW, NW = L::NW;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  const int K = a.k, segcap = a.segcap;
+  double* const sd = reinterpret_cast<double*>(smraw);  // exchange line; output staging
+  T* const stg = reinterpret_cast<T*>(sd + CAP);        // input staging (next plane's row)
+  double* const wtA = sd + 2 * CAP;
+  double* const wtB = wtA + NW;
+  double* const zc = wtB + NW;                         // [2K][segcap]
+  double* const hist = zc + size_t(2) * K * segcap;    // [2K][segcap]
+  int2* const sseg = reinterpret_cast<int2*>(hist + size_t(2) * K * segcap);
+  uint64_t* const mw = reinterpret_cast<uint64_t*>(sseg + segcap);
+  uint64_t* const bar = mw + MWW;
+
+  const int n = a.n, nl = a.nl;
+  const int64_t nh = int64_t(n) * nl;
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t groups = (planes + a.planes_per_cta - 1) / a.planes_per_cta;
+  const int64_t line = blockIdx.x / groups, grp = blockIdx.x - line * groups;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int p0 = tid * V;
+  const uint32_t sdb = smem_u32(sd + p0);  // this thread's chunk in the exchange line
+  constexpr uint64_t VM = (1ull << V) - 1ull;
+  const uint32_t rowbytes = static_cast<uint32_t>(n) * sizeof(T);
+  // bulk (TMA) row copies need 16 B aligned rows
+  const bool bulk = (rowbytes % 16 == 0) && ((reinterpret_cast<uintptr_t>(in) |
+                                               reinterpret_cast<uintptr_t>(out)) % 16 == 0);
+
+  const int64_t pl_begin = grp * a.planes_per_cta;
+  const int64_t pl_end = pl_begin + a.planes_per_cta < planes ? pl_begin + a.planes_per_cta : planes;
+
+  auto fetch = [&](int64_t pl) {  // start the row of plane pl towards the staging buffer
+    const T* src = in + pl * nh + line * n;
+    if (bulk) {
+      if (tid == 0) {
+        mbar_arrive_expect_tx(bar, rowbytes);
+        bulk_g2s(stg, src, rowbytes, bar);
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const int i = tid + u * NT;
+        if (i < n) rf1l_cp_async(stg + i, src + i, sizeof(T));
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
+    }
+  };
+  if (tid == 0) {
+    mbar_init(bar, 1);
+    mbar_fence_init();
+  }
+  __syncthreads();
+  fetch(pl_begin);
+
+  uint32_t live = 0, starts = 0, ends = 0, slotL = 0, slotR = 0, seab = 0;
+  double la[V];
+  double A = 1.0;
+  int nseg = 0;
+  uint32_t phase = 0;
+  for (int64_t pl = pl_begin; pl < pl_end; ++pl) {
+    const int64_t var = pl / a.nlev, lev = a.lev0 + (pl - var * a.nlev);
+    const bool reuse = pl > pl_begin && pl - var * a.nlev > 0 && a.same[lev];
+    if (!reuse) {
+      // ---- chunk masks and links, mask words, segments and zone responses
+      const uint64_t* Wl = a.bits + (lev * nl + line) * a.words;
+      const int G = a.ghost[lev];
+      const uint64_t win =
+          p0 > 0 ? rf1l_window(Wl, a.words, p0 - 1) : (rf1l_window(Wl, a.words, 0) << 1);
+      const uint64_t sea = (win >> 1) & VM, prv = win & VM, nxt = (win >> 2) & VM;
+      const uint64_t frozen = G == 0 ? (sea & ~prv & ~nxt) : 0ull;  // covariance.cpp:260-269
+      seab = static_cast<uint32_t>(sea);
+      live = static_cast<uint32_t>(sea & ~frozen);
+      starts = static_cast<uint32_t>(sea & ~prv);
+      ends = static_cast<uint32_t>(sea & ~nxt);
+      slotL = static_cast<uint32_t>(~sea & nxt & VM);  // land before a segment start
+      // land after a segment end; none past the line (a segment ending at the
+      // last point has no right ghosts, and nothing places a value there)
+      const int inl = n - p0;
+      const uint64_t inm = inl >= V ? VM : (inl > 0 ? (1ull << inl) - 1ull : 0ull);
+      slotR = static_cast<uint32_t>(~sea & prv & inm);
+      {
+        const double* cp = reinterpret_cast<const double*>(a.c1 + line * a.csl + p0 * a.csp);
+        const int64_t cst = 2 * a.csp;
+#pragma unroll
+        for (int i = 0; i < V; ++i) {
+          double al = 0.0;
+          if ((live >> i) & 1u) al = __ldg(cp + i * cst);
+          la[i] = al;
+        }
+      }
+      A = 1.0;
+#pragma unroll
+      for (int i = 0; i < V; ++i) A *= la[i];
+      for (int w = tid; w < MWW; w += NT) mw[w] = w < a.words ? ldw(Wl, w) : 0ull;
+      const int64_t sb0 = a.seg_off[lev * nl + line];
+      nseg = static_cast<int>(a.seg_off[lev * nl + line + 1] - sb0);
+      for (int s = tid; s < nseg; s += NT) {
+        sseg[s] = a.segs[sb0 + s];
+        for (int d = 0; d < 2 * K; ++d) zc[d * segcap + s] = __ldg(a.zone + d * a.nsegs + sb0 + s);
+      }
+    }
+
+    // ---- this plane's row: staging -> registers (land = 0, adjoint input scaling)
+    if (bulk) {
+      mbar_wait(bar, phase);
+      phase ^= 1u;
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    double v[V];
+    {
+      const double* pre = (TR && a.pre_scale) ? a.pre_scale + lev * nh + line * n + p0 : nullptr;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        double x = static_cast<double>(stg[p0 + i]);
+        if (TR) {
+          if (pre && ((seab >> i) & 1u)) x *= __ldg(pre + i);
+        }
+        v[i] = ((seab >> i) & 1u) ? x : 0.0;
+      }
+    }
+    __syncthreads();  // the staging buffer is free
+    if (pl + 1 < pl_end) fetch(pl + 1);
+    // the previous plane's bulk store must have read the exchange line before
+    // this plane's first exit is published (after the first pass's barrier)
+    if (bulk && tid == 0) bulk_wait_read_all();
+
+    // ---- one pass
+    auto pass = [&](auto asc_c, auto first_c, auto last_c, auto pull_c) {
+      constexpr bool ASC = decltype(asc_c)::value;
+      constexpr bool FIRST = decltype(first_c)::value;  // adjoint: raw input
+      constexpr bool LAST = decltype(last_c)::value;    // adjoint: b_i on the output
+      constexpr bool PULL = decltype(pull_c)::value;    // entries were placed for this pass
+      const uint32_t slots = ASC ? slotL : slotR;       // land slots holding this pass's entries
+      const uint32_t exits = ASC ? ends : starts;       // states handed to the zones
+      double r = 0.0;
+#pragma unroll
+      for (int ii = 0; ii < V; ++ii) {
+        const int i = ASC ? ii : V - 1 - ii;
+        if constexpr (PULL) rf1l_lds_if(v[i], sdb + 8u * i, slots & (1u << i));
+        double t;
+        if constexpr (!TR) {
+          t = fma(-la[i], v[i], v[i]);  // b_i s_i with b = 1 - a; a land slot keeps its value
+        } else {
+          const double w = FIRST ? v[i] : fma(-la[i], v[i], v[i]);
+          t = ((live >> i) & 1u) ? la[i] * w : v[i];
+        }
+        r = fma(la[i], r, t);
+      }
+      // inclusive scan of (A, r) over the warp's lanes in pass order
+      const int pos = ASC ? lane : 31 - lane;
+      double ar = A, br = r;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const double ua = ASC ? __shfl_up_sync(0xffffffffu, ar, d) : __shfl_down_sync(0xffffffffu, ar, d);
+        const double ub = ASC ? __shfl_up_sync(0xffffffffu, br, d) : __shfl_down_sync(0xffffffffu, br, d);
+        if (pos >= d) {
+          br = fma(ar, ub, br);
+          ar *= ua;
+        }
+      }
+      double ae = ASC ? __shfl_up_sync(0xffffffffu, ar, 1) : __shfl_down_sync(0xffffffffu, ar, 1);
+      double be = ASC ? __shfl_up_sync(0xffffffffu, br, 1) : __shfl_down_sync(0xffffffffu, br, 1);
+      if (pos == 0) {
+        ae = 1.0;
+        be = 0.0;
+      }
+      if (pos == 31) {
+        wtA[warp] = ar;
+        wtB[warp] = br;
+      }
+      __syncthreads();
+      double cw = 0.0;  // state entering this warp: fold the totals of the warps before it
+#pragma unroll
+      for (int k2 = 0; k2 < NW; ++k2) {
+        const int w2 = ASC ? k2 : NW - 1 - k2;
+        const double ta = wtA[w2], tb = wtB[w2];
+        if (ASC ? w2 < warp : w2 > warp) cw = fma(ta, cw, tb);
+      }
+      r = fma(ae, cw, be);
+#pragma unroll
+      for (int ii = 0; ii < V; ++ii) {
+        const int i = ASC ? ii : V - 1 - ii;
+        if constexpr (!TR) {
+          r = fma(la[i], r, fma(-la[i], v[i], v[i]));
+          v[i] = r;
+          rf1l_sts_if(sdb + 8u * i, r, exits & (1u << i));
+        } else {
+          const bool on = (live >> i) & 1u;
+          const double w = FIRST ? v[i] : fma(-la[i], v[i], v[i]);
+          const double cur = w + r;  // cur_i = w_i + a_{i-1} cur_{i-1}
+          r = fma(la[i], r, on ? la[i] * w : v[i]);
+          if (on) v[i] = LAST ? fma(-la[i], cur, cur) : cur;
+          rf1l_sts_if(sdb + 8u * i, cur, exits & (1u << i));
+        }
+      }
+      __syncthreads();
+    };
+
+    // ---- between passes: record exits, place the next entries
+    auto boundary = [&](bool after_asc, int it) {
+      for (int s = tid; s < nseg; s += NT) {
+        const int2 sg = sseg[s];
+        const int i0 = sg.x, j0 = sg.x + sg.y - 1;
+        if (after_asc) {
+          hist[(K + it - 1) * segcap + s] = sd[j0];
+          if (j0 < n - 1) {
+            double e = 0.0;
+            for (int j = 1; j <= it; ++j)
+              e = fma(zc[(K + it - j) * segcap + s], hist[(K + j - 1) * segcap + s], e);
+            if (TR) e *= __ldg(&a.c1[line * a.csl + j0 * a.csp].x);
+            sd[j0 + 1] = e;
+          }
+        } else {
+          hist[(it - 1) * segcap + s] = sd[i0];
+          if (i0 > 0) {
+            double e = 0.0;
+            for (int j = 1; j <= it; ++j) e = fma(zc[(it + 1 - j) * segcap + s], hist[(j - 1) * segcap + s], e);
+            if (TR) e *= __ldg(&a.c1[line * a.csl + i0 * a.csp].x);
+            sd[i0 - 1] = e;
+          }
+        }
+      }
+      __syncthreads();
+    };
+
+    using Tt = std::true_type;
+    using Ft = std::false_type;
+    for (int it = 1; it <= K; ++it) {
+      // iteration 1 enters every segment from zero: no entries to pull
+      if (it == 1) pass(Tt{}, std::integral_constant<bool, TR>{}, Ft{}, Ft{});
+      else pass(Tt{}, Ft{}, Ft{}, Tt{});
+      boundary(true, it);
+      if (TR && it == K) pass(Ft{}, Ft{}, Tt{}, Tt{}); else pass(Ft{}, Ft{}, Ft{}, Tt{});
+      if (it < K) boundary(false, it);
+    }
+
+    // ---- publish the chunks (land exactly 0, output scaling) and store the row
+    {
+      T* const ost = reinterpret_cast<T*>(sd);
+      const double* post = a.post_scale ? a.post_scale + lev * nh + line * n + p0 : nullptr;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        double o = ((seab >> i) & 1u) ? v[i] : 0.0;
+        if (post && ((seab >> i) & 1u)) o *= __ldg(post + i);
+        ost[p0 + i] = static_cast<T>(o);
+      }
+      T* dst = out + pl * nh + line * n;
+      if (bulk) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+          bulk_s2g(dst, ost, rowbytes);
+          bulk_commit();
+        }
+      } else {
+        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < V; ++u) {
+          const int i = tid + u * NT;
+          if (i < n) dst[i] = ost[i];
+        }
+        __syncthreads();  // the next plane's passes write the exchange line
+      }
+    }
+  }
+  if (bulk && tid == 0) bulk_wait_all();
+}
+
+template <typename T, bool TR, int NT, int V, int MINB>
+bool rf1_row_launch_shape(const T* in, T* out, const Rf1RowArgs& a, cudaStream_t st) {
+  using L = Rf1RowSmem<NT, V>;
+  const size_t smem = L::bytes(a.k, a.segcap);
+  if (smem > 227 * 1024 / MINB) return false;
+  auto kern = k_rf1_row<T, TR, NT, V, MINB>;
+  static size_t attr = 0;
+  if (smem > attr) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             static_cast<int>(smem)) != cudaSuccess)
+      return false;
+    attr = smem;
+  }
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t groups = (planes + a.planes_per_cta - 1) / a.planes_per_cta;
+  kern<<<static_cast<unsigned>(int64_t(a.nl) * groups), NT, smem, st>>>(in, out, a);
+  return true;
+}
+
+// rows of up to 8704 points; false: the caller falls back
+template <typename T, bool TR>
+bool launch_rf1_row_tr(const T* in, T* out, Rf1RowArgs a, cudaStream_t st) {
+  const int64_t planes = a.nvar * a.nlev;
+  int ppc = static_cast<int>(std::max<int64_t>(1, int64_t(a.nl) * planes / (148 * 4 * 4)));
+  a.planes_per_cta = static_cast<int>(std::min<int64_t>(std::min<int64_t>(ppc, 16), planes));
+  if (a.n <= 128 * 9) return rf1_row_launch_shape<T, TR, 128, 9, 4>(in, out, a, st);
+  if (a.n <= 128 * 17) return rf1_row_launch_shape<T, TR, 128, 17, 4>(in, out, a, st);
+  if (a.n <= 256 * 17) return rf1_row_launch_shape<T, TR, 256, 17, 2>(in, out, a, st);
+  if (a.n <= 512 * 17) return rf1_row_launch_shape<T, TR, 512, 17, 1>(in, out, a, st);
+  return false;
+}
+template <typename T>
+bool launch_rf1_row(const T* in, T* out, const Rf1RowArgs& a, cudaStream_t st) {
+  return a.transpose ? launch_rf1_row_tr<T, true>(in, out, a, st)
+                     : launch_rf1_row_tr<T, false>(in, out, a, st);
+}
+
 // ------------------------------------------------------------- launcher
 // shapes: x lines NT=128 (4 CTAs/SM), y tiles of 64 B rows NT=512 (1 CTA/SM)
 template <typename T, typename S, bool TR, int NT, int V, int C, int MINB>
@@ -392,6 +778,31 @@ bool rf1_line_launch_v(const T* in, T* out, const Rf1LineArgs& a, cudaStream_t s
 template <typename T>
 bool launch_rf1_line(const T* in, T* out, Rf1LineArgs a, cudaStream_t st) {
   const int64_t planes = a.nvar * a.nlev;
+  if (a.dir == 0 && a.nx <= 512 * 17) {
+    Rf1RowArgs r{};
+    r.transpose = a.transpose;
+    r.k = a.k;
+    r.n = static_cast<int>(a.nx);
+    r.nl = static_cast<int>(a.ny);
+    r.nlev = a.nlev;
+    r.nvar = a.nvar;
+    r.lev0 = a.lev0;
+    r.c1 = a.c1;
+    r.csp = 1;
+    r.csl = a.nx;
+    r.bits = a.bits;
+    r.words = a.words;
+    r.seg_off = a.seg_off;
+    r.segs = a.segs;
+    r.nsegs = a.nsegs;
+    r.zone = a.zone;
+    r.ghost = a.ghost;
+    r.same = a.same;
+    r.pre_scale = a.pre_scale;
+    r.post_scale = a.post_scale;
+    r.segcap = a.segcap;
+    if (launch_rf1_row<T>(in, out, r, st)) return true;
+  }
   if (a.dir == 0) {
     const int64_t nl = a.ny;
     // enough CTAs for ~4 waves of 148 x 4

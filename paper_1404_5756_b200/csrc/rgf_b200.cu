@@ -184,6 +184,7 @@ struct rgf_op {
   // planes): default on; RGF_B200_XT=0 at creation turns it off
   bool xt_mode = true;
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
+  DevBuf<uint8_t> mask_same;  // per level: mask and ghost width equal the previous level's
   bool rf1_line = true;  // line-resident 1st-RF sweeps (RGF_B200_RF1LINE=0 at creation: streaming)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
@@ -575,6 +576,7 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
       b.nsegs = d.nsegs;
       b.zone = a.zone;
       b.ghost = op->ghost_d.p;
+      b.same = op->mask_same.p;
       b.pre_scale = pre;
       b.post_scale = post;
       b.segcap = std::max(1, d.segcap);
@@ -1553,6 +1555,20 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         CUDA_OK(cudaDeviceSynchronize());
         op->rf1_ok = true;
         if (const char* le = std::getenv("RGF_B200_RF1LINE")) op->rf1_line = le[0] != '0';
+        {
+          std::vector<uint8_t> same(static_cast<size_t>(g->nlev), 1);
+          same[0] = 0;
+          op->mask_same.upload(same.data(), same.size());
+          if (g->nlev > 1) {
+            rgfb::k_mask_same<<<grid_for(nh * (g->nlev - 1), 256, 148 * 32), 256>>>(
+                mask.p, nh, g->nlev, op->mask_same.p);
+            CUDA_OK(cudaGetLastError());
+            CUDA_OK(cudaMemcpy(same.data(), op->mask_same.p, same.size(), cudaMemcpyDeviceToHost));
+            for (int64_t l = 1; l < g->nlev; ++l)
+              if (op->ghost[l] != op->ghost[l - 1]) same[static_cast<size_t>(l)] = 0;
+            op->mask_same.upload(same.data(), same.size());
+          }
+        }
         for (int dir = 0; dir < 2; ++dir) {
           DirData& d = dir == 0 ? op->dx_ : op->dy_;
           int64_t cap = 0;
