@@ -185,6 +185,7 @@ struct rgf_op {
   bool xt_mode = true;
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
   DevBuf<uint8_t> mask_same;  // per level: mask and ghost width equal the previous level's
+  bool rf1_stream = true;  // streaming passes usable (every level has ghosts)
   bool rf1_line = true;  // line-resident 1st-RF sweeps (RGF_B200_RF1LINE=0 at creation: streaming)
   DevBuf<double> rf1_hist;  // [var][segment][2K] boundary states (apply scratch)
   DevBuf<double> rf1_ent;   // [var][segment] entry states of the current pass
@@ -587,16 +588,18 @@ void sweep(rgf_op* op, int dir, bool transpose, const T* in, T* out, int64_t nva
         return;
       }
     }
-    op->rf1_hist.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs * 2 * op->k)));
-    a.hist = op->rf1_hist.p;
-    op->rf1_ent.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs)));
-    a.ent = op->rf1_ent.p;
-    a.pre_scale = pre;
-    a.post_scale = post;
-    op->launches += static_cast<unsigned long long>(rgfb::launch_rf1_sweep<T>(in, out, a, st));
-    CUDA_OK(cudaGetLastError());
-    RGF_DEBUG_SYNC(st, "rf1 sweep");
-    return;
+    if (op->rf1_stream) {
+      op->rf1_hist.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs * 2 * op->k)));
+      a.hist = op->rf1_hist.p;
+      op->rf1_ent.alloc(static_cast<size_t>(std::max<int64_t>(1, nvar * d.nsegs)));
+      a.ent = op->rf1_ent.p;
+      a.pre_scale = pre;
+      a.post_scale = post;
+      op->launches += static_cast<unsigned long long>(rgfb::launch_rf1_sweep<T>(in, out, a, st));
+      CUDA_OK(cudaGetLastError());
+      RGF_DEBUG_SYNC(st, "rf1 sweep");
+      return;
+    }
   }
 
   const int64_t n = dir == 0 ? op->nx : op->ny;
@@ -1555,6 +1558,10 @@ int rgf_op_create(const rgf_grid_desc* g, const double* rx, const double* ry,
         CUDA_OK(cudaDeviceSynchronize());
         op->rf1_ok = true;
         if (const char* le = std::getenv("RGF_B200_RF1LINE")) op->rf1_line = le[0] != '0';
+        // the streaming passes assume ghost zones on every side that meets
+        // land; without ghosts (ghost_width = 0) lines that do not fit the
+        // resident kernel take the segment-serial kernel
+        op->rf1_stream = *std::min_element(op->ghost.begin(), op->ghost.end()) > 0;
         {
           std::vector<uint8_t> same(static_cast<size_t>(g->nlev), 1);
           same[0] = 0;

@@ -410,12 +410,15 @@ def test_unaligned_rows_device_path_pitched(P, nx, dt):
 
 @pytest.mark.parametrize("k", [1, 2, 5])
 def test_rf1_streaming_path(P, monkeypatch, k):
-    """The 1st-RF runs as 2K streaming passes per sweep (ghost zones folded
-    into per-segment convolutions), against the oracle and against the
-    segment-serial exact kernel (RGF_B200_EXACT=1, reference arithmetic)."""
+    """RGF_B200_RF1LINE=0: the 1st-RF as 2K streaming passes per sweep (ghost
+    zones folded into per-segment convolutions), against the oracle and
+    against the segment-serial exact kernel (RGF_B200_EXACT=1, reference
+    arithmetic). It is the fallback of the line-resident kernel."""
     g, rx, ry = random_case(800 + k, nx=70, ny=44, nlev=3, sea=0.65)
     var = np.random.default_rng(17).uniform(0.5, 2.0, (3, 44, 70))
+    monkeypatch.setenv("RGF_B200_RF1LINE", "0")
     gpu, cpu = build_pair(P, g, rx, ry, order=1, k=k, variance=var)
+    monkeypatch.delenv("RGF_B200_RF1LINE")
     monkeypatch.setenv("RGF_B200_EXACT", "1")
     exact, _ = build_pair(P, g, rx, ry, order=1, k=k, variance=var)
     monkeypatch.delenv("RGF_B200_EXACT")
@@ -433,6 +436,71 @@ def test_rf1_streaming_path(P, monkeypatch, k):
         want = cpu.apply(getattr(O, name), f)
         assert relmax(got, want) <= TOL64, (name, relmax(got, want))
         assert relmax(got, exact.apply(getattr(P, name), f)) <= TOL64, name
+
+
+@pytest.mark.parametrize("k,nx,ny,ghost", [(1, 70, 44, None), (2, 57, 43, None), (5, 70, 44, None),
+                                           (5, 96, 40, 0), (3, 64, 50, 2), (5, 300, 200, None)])
+def test_rf1_line_resident_path(P, monkeypatch, k, nx, ny, ghost):
+    """The default 1st-RF path (rf1_line.cuh): one launch per sweep runs all K
+    iterations with the line resident on chip, each pass a parallel scan.
+    Every kind in fp64 and fp32 against the oracle and the exact kernel;
+    ghost_width = 0 covers the pass-through of isolated points
+    (covariance.cpp:260-269); nx = 57 rows are not 16 B aligned (cp.async
+    pieces instead of bulk copies)."""
+    g, rx, ry = random_case(900 + k + nx, nx=nx, ny=ny, nlev=3, sea=0.65)
+    var = np.random.default_rng(17).uniform(0.5, 2.0, (3, ny, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, order=1, k=k, variance=var, ghost=ghost)
+    monkeypatch.setenv("RGF_B200_EXACT", "1")
+    exact, _ = build_pair(P, g, rx, ry, order=1, k=k, variance=var, ghost=ghost)
+    monkeypatch.delenv("RGF_B200_EXACT")
+    import torch
+    f = np.random.default_rng(18).standard_normal((2, 3, ny, nx))
+    ft = torch.from_numpy(f).cuda()
+    land = ~g["mask"]
+    for name in KINDS:
+        l0 = gpu.launch_count()
+        dev = gpu.apply(getattr(P, name), ft)
+        torch.cuda.synchronize()
+        sweeps = {"GX": 1, "GY": 1, "GXT": 1, "GYT": 1, "V": 2, "VT": 2, "B": 4, "GYGX": 2}[name]
+        assert gpu.launch_count() - l0 == sweeps, (name, gpu.launch_count() - l0)
+        want = cpu.apply(getattr(O, name), f)
+        got = dev.cpu().numpy()
+        assert relmax(got, want) <= TOL64, (name, relmax(got, want))
+        assert np.all(got[:, land] == 0.0), name
+        assert relmax(got, exact.apply(getattr(P, name), f)) <= TOL64, name
+        assert np.array_equal(gpu.apply(getattr(P, name), f), got), name  # host pipeline
+    f32 = f.astype(np.float32)
+    for name in ("GYGX", "VT", "B"):
+        got = gpu.apply(getattr(P, name), f32)
+        want = cpu.apply(getattr(O, name), f32.astype(np.float64))
+        assert got.dtype == np.float32 and relmax(got, want) <= TOL32, (name, relmax(got, want))
+
+
+def test_rf1_line_resident_shared_masks_and_long_lines(P):
+    """Levels with one mask reuse a CTA's links, masks and zone tables from
+    plane to plane (several planes per CTA, the next plane's row prefetched);
+    a 4400-point row takes the 512-thread shape and a 2300-row column does
+    not fit the resident shapes (streaming fallback for that direction)."""
+    rng = np.random.default_rng(31)
+    nx, ny, nlev = 64, 1300, 6
+    g = uniform_grid(nx, ny, 5000.0, 7000.0, nlev=nlev)
+    g["mask"] = np.repeat(checkered_mask(nx, ny, 5, 0.7, nlev=1), nlev, axis=0)
+    rx = g["dx"] * rng.uniform(1.2, 4.5, (ny, nx))
+    ry = g["dy"] * rng.uniform(1.2, 4.5, (ny, nx))
+    gpu, cpu = build_pair(P, g, rx, ry, order=1, k=5)
+    f = rng.standard_normal((1, nlev, ny, nx))
+    for name in ("GYGX", "VT"):
+        assert relmax(gpu.apply(getattr(P, name), f), cpu.apply(getattr(O, name), f)) <= TOL64, name
+    for nx, ny in ((4400, 24), (40, 2300)):
+        g = uniform_grid(nx, ny, 5000.0, 7000.0, nlev=2)
+        g["mask"] = checkered_mask(nx, ny, 9, 0.8, nlev=2)
+        rx = g["dx"] * rng.uniform(1.2, 6.0, (ny, nx))
+        ry = g["dy"] * rng.uniform(1.2, 6.0, (ny, nx))
+        gpu, cpu = build_pair(P, g, rx, ry, order=1, k=3)
+        f = rng.standard_normal((1, 2, ny, nx))
+        for name in ("GYGX", "VT"):
+            assert relmax(gpu.apply(getattr(P, name), f), cpu.apply(getattr(O, name), f)) <= TOL64, \
+                (nx, ny, name)
 
 
 @pytest.mark.parametrize("nx,dt", [(96, "f64"), (160, "f32"), (64, "f64")])
