@@ -208,7 +208,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
 
   uint32_t live = 0, starts = 0, ends = 0, slotL = 0, slotR = 0, seab = 0;
   double la[V];
-  double A = 1.0;
+  double A = 1.0;  // the chunk's link product
   uint32_t phase = 0;
   for (int64_t pl = pl_begin; pl < pl_end; ++pl) {
     const int64_t var = pl / a.nlev, lev = a.lev0 + (pl - var * a.nlev);
@@ -298,19 +298,25 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
       constexpr bool PULL = decltype(pull_c)::value;    // entries were placed for this pass
       const uint32_t slots = ASC ? slotL : slotR;       // land slots holding this pass's entries
       const uint32_t exits = ASC ? ends : starts;       // states handed to the zones
-      double r = 0.0;
+      // input term of point i (and, adjoint, its input w_i). `again`: second
+      // walk of the pass (a forward value pulled in the first walk is kept)
+      auto term = [&](int i, double& w, bool again) -> double {
+        if constexpr (!TR) {
+          if (PULL && !again) rf1l_lds_if(v[i], sdb + SST * i, slots & (1u << i));
+          w = 0.0;
+          return fma(-la[i], v[i], v[i]);  // b_i s_i with b = 1 - a; a land slot keeps its value
+        } else {
+          double e = 0.0;  // entry placed in this land slot (z-type: a_s E)
+          if constexpr (PULL) rf1l_lds_if(e, sdb + SST * i, slots & (1u << i));
+          w = FIRST ? v[i] : fma(-la[i], v[i], v[i]);
+          return fma(la[i], w, e);
+        }
+      };
+      double r = 0.0, wdummy;
 #pragma unroll
       for (int ii = 0; ii < V; ++ii) {
         const int i = ASC ? ii : V - 1 - ii;
-        if constexpr (PULL) rf1l_lds_if(v[i], sdb + SST * i, slots & (1u << i));
-        double t;
-        if constexpr (!TR) {
-          t = fma(-la[i], v[i], v[i]);  // b_i s_i with b = 1 - a; a land slot keeps its value
-        } else {
-          const double w = FIRST ? v[i] : fma(-la[i], v[i], v[i]);
-          t = ((live >> i) & 1u) ? la[i] * w : v[i];
-        }
-        r = fma(la[i], r, t);
+        r = fma(la[i], r, term(i, wdummy, false));
       }
       // inclusive scan of (A, r) over the line's chunks in this warp, in pass order
       const int pos = ASC ? lane / C : QW - 1 - lane / C;
@@ -342,20 +348,21 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
         const double ta = wtA[w2 * C + c], tb = wtB[w2 * C + c];
         if (ASC ? w2 < warp : w2 > warp) cw = fma(ta, cw, tb);
       }
-      r = fma(ae, cw, be);
+      r = fma(ae, cw, be);  // state entering the chunk
 #pragma unroll
       for (int ii = 0; ii < V; ++ii) {
         const int i = ASC ? ii : V - 1 - ii;
+        double w;
+        const double t = term(i, w, true);
         if constexpr (!TR) {
-          r = fma(la[i], r, fma(-la[i], v[i], v[i]));
+          r = fma(la[i], r, t);
           v[i] = r;
           rf1l_sts_if(sdb + SST * i, r, exits & (1u << i));
         } else {
-          const bool on = (live >> i) & 1u;
-          const double w = FIRST ? v[i] : fma(-la[i], v[i], v[i]);
           const double cur = w + r;  // cur_i = w_i + a_{i-1} cur_{i-1}
-          r = fma(la[i], r, on ? la[i] * w : v[i]);
-          if (on) v[i] = LAST ? fma(-la[i], cur, cur) : cur;
+          r = fma(la[i], r, t);
+          // land values are never read back into sea points (their link is 0)
+          v[i] = LAST ? fma(-la[i], cur, cur) : cur;
           rf1l_sts_if(sdb + SST * i, cur, exits & (1u << i));
         }
       }
@@ -481,15 +488,19 @@ bool launch_rf1_line_tr(const T* in, T* out, Rf1LineArgs a, cudaStream_t st) {
     if (n <= 512 * 17) return rf1_res_launch_shape<T, TR, 512, 17, 1, 1>(in, out, a, st);
     return false;
   }
-  // columns: tiles of 4 adjacent columns (32 B row pieces in fp64), up to 2176 rows
-  constexpr int CY = 4;
+  // columns: tiles of 2 adjacent columns (16 B row pieces in fp64; the other
+  // half of each 32 B sector belongs to the neighbouring tile, whose CTA runs
+  // in the same wave), up to 2176 rows. Measured on C5 (20 levels, fp64 y
+  // sweep): 2 columns x 256 threads, two CTAs per SM 2.93 ms; 4 columns x 512
+  // threads, one CTA per SM 3.20 ms.
+  constexpr int CY = 2;
   const int64_t n = a.ny, tiles = (a.nx + CY - 1) / CY;
   int ppc = static_cast<int>(std::max<int64_t>(1, tiles * planes / (148 * 4 * 2)));
   a.planes_per_cta = static_cast<int>(std::min<int64_t>(std::min<int64_t>(ppc, 16), planes));
-  if (n <= 32 * 9) return rf1_res_launch_shape<T, TR, 128, 9, CY, 4>(in, out, a, st);
-  if (n <= 64 * 9) return rf1_res_launch_shape<T, TR, 256, 9, CY, 2>(in, out, a, st);
-  if (n <= 64 * 17) return rf1_res_launch_shape<T, TR, 256, 17, CY, 2>(in, out, a, st);
-  if (n <= 128 * 17) return rf1_res_launch_shape<T, TR, 512, 17, CY, 1>(in, out, a, st);
+  if (n <= 32 * 9) return rf1_res_launch_shape<T, TR, 64, 9, CY, 4>(in, out, a, st);
+  if (n <= 64 * 9) return rf1_res_launch_shape<T, TR, 128, 9, CY, 4>(in, out, a, st);
+  if (n <= 64 * 17) return rf1_res_launch_shape<T, TR, 128, 17, CY, 4>(in, out, a, st);
+  if (n <= 128 * 17) return rf1_res_launch_shape<T, TR, 256, 17, CY, 2>(in, out, a, st);
   return false;
 }
 
