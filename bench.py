@@ -445,15 +445,19 @@ def main():
 
         m_adj = timed(sop.op, P.VT, x, y)
         extra["3rd-RF adjoint VT f64"] = entry(m_adj, 3, 8)
-        for label, o2, k2, dt2, w2 in (("1st-RF K=5 f64", 1, 5, torch.float64, 8),
-                                       ("3rd-RF f32", 3, 1, torch.float32, 4)):
+        for o2, k2, cases in ((1, 5, (("1st-RF K=5 f64", torch.float64, 8, P.GYGX),
+                                       ("1st-RF K=5 adjoint VT f64", torch.float64, 8, P.VT),
+                                       ("1st-RF K=5 f32", torch.float32, 4, P.GYGX))),
+                              (3, 1, (("3rd-RF f32", torch.float32, 4, P.GYGX),))):
             op2 = P.HorizontalCovarianceOp(grid, P.ScaleField(cfg.rx, cfg.ry),
                                            P.CovarianceOptions(order=P.FilterOrder(o2),
                                                                k_iterations=k2, device=local))
-            x2 = x.to(dt2)
-            y2 = torch.empty_like(x2)
-            extra[label] = entry(timed(op2, P.GYGX, x2, y2), o2, w2)
-            del op2, x2, y2
+            for label, dt2, w2, kind2 in cases:
+                x2 = x.to(dt2)
+                y2 = torch.empty_like(x2)
+                extra[label] = entry(timed(op2, kind2, x2, y2), o2, w2)
+                del x2, y2
+            del op2
         extra["t(1st-RF K=5)/t(3rd-RF)"] = extra["1st-RF K=5 f64"]["ms"] / ms
 
     cpu = cpu1 = None
