@@ -26,10 +26,10 @@
 //     previous state. No per-point segment logic in the passes.
 //   * Shared memory holds an exchange copy of the line that is touched only
 //     where a value changes hands: a segment's exit point is published
-//     (predicated store), one thread per segment records it (x_it at the
-//     start, y_it at the end), evaluates the zone convolution from the
-//     histories and places the next entry, and the owner of that land slot
-//     pulls it (predicated load) at the start of the next pass.
+//     (predicated store), one thread per segment takes it (x_it at the start,
+//     y_it at the end), adds its zone response to the pending entries of the
+//     coming iterations and places the next entry, and the owner of that land
+//     slot pulls it (predicated load) at the start of the next pass.
 //   * The adjoint passes cur_i = w_i + a_{i-1} cur_{i-1}, out = b_i cur_i
 //     run on z_i = a_i cur_i (z_i = a_i z_{i-1} + a_i w_i: the same links),
 //     with cur_i = w_i + z_{i-1} stored and the b_i factor applied to the
@@ -115,7 +115,8 @@ struct Rf1ResSmem {
   static size_t bytes(int K, int segcap) {
     size_t b = size_t(2) * CAP * C * sizeof(double);    // exchange lines + input staging
     b += size_t(2) * NW * C * sizeof(double);           // warp totals
-    b += size_t(4) * K * C * segcap * sizeof(double);   // zone cache + histories
+    b += size_t(4) * K * C * segcap * sizeof(double);   // zone cache + pending entries
+    b += size_t(2) * C * segcap * sizeof(double);       // alpha at segment starts / ends
     b += size_t(C) * segcap * sizeof(int2);
     b += size_t(C) * sizeof(int) + 16;                  // segments per line, mbarrier
     return b;
@@ -140,8 +141,9 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
   double* const wtA = sd + 2 * CAP * C;                 // [NW][C]
   double* const wtB = wtA + NW * C;
   double* const zc = wtB + NW * C;                          // [2K][C*segcap]
-  double* const hist = zc + size_t(2) * K * C * segcap;     // [2K][C*segcap]
-  int2* const sseg = reinterpret_cast<int2*>(hist + size_t(2) * K * C * segcap);  // [C][segcap]
+  double* const acc = zc + size_t(2) * K * C * segcap;      // [2K][C*segcap]: pending entries
+  double* const salpha = acc + size_t(2) * K * C * segcap;  // [2][C*segcap]: alpha at start / end
+  int2* const sseg = reinterpret_cast<int2*>(salpha + size_t(2) * C * segcap);  // [C][segcap]
   int* const scnt = reinterpret_cast<int*>(sseg + size_t(C) * segcap);
   uint64_t* const bar = reinterpret_cast<uint64_t*>(
       (reinterpret_cast<uintptr_t>(scnt + C) + 7) & ~uintptr_t(7));
@@ -152,7 +154,12 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
   const int64_t gsp = XD ? 1 : nl, gsl = XD ? n : 1;   // field/coefficient strides (point, line)
   const int64_t planes = a.nvar * a.nlev;
   const int64_t groups = (planes + a.planes_per_cta - 1) / a.planes_per_cta;
-  const int64_t tile = blockIdx.x / groups, grp = blockIdx.x - tile * groups;
+  // y tiles come in cluster pairs: the two CTAs of a cluster own neighbouring
+  // tiles (the two halves of each 32 B sector) and keep step plane by plane,
+  // so their loads and stores of a sector meet in L2
+  const int64_t unit = C > 1 ? blockIdx.x / 2 : blockIdx.x;
+  const int64_t upos = unit / groups, grp = unit - upos * groups;
+  const int64_t tile = C > 1 ? 2 * upos + (blockIdx.x & 1) : upos;
   const int line0 = static_cast<int>(tile) * C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int c = tid % C, q = tid / C;
@@ -256,9 +263,15 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
         const int ns = static_cast<int>(a.seg_off[lev * nl + line0 + cc + 1] - sb0);
         if (tid == 0) scnt[cc] = ns;
         for (int s = tid; s < ns; s += NT) {
-          sseg[cc * segcap + s] = a.segs[sb0 + s];
+          const int2 sg = a.segs[sb0 + s];
+          sseg[cc * segcap + s] = sg;
           for (int d = 0; d < 2 * K; ++d)
             zc[(d * C + cc) * segcap + s] = __ldg(a.zone + d * a.nsegs + sb0 + s);
+          if (TR) {  // the adjoint's entries are scaled by the end point's alpha
+            const double2* cl = a.c1 + (line0 + cc) * gsl;
+            salpha[cc * segcap + s] = __ldg(&cl[sg.x * gsp].x);
+            salpha[C * segcap + cc * segcap + s] = __ldg(&cl[(sg.x + sg.y - 1) * gsp].x);
+          }
         }
       }
     }
@@ -285,6 +298,10 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
       }
     }
     __syncthreads();  // the staging buffer is free
+    if constexpr (C > 1) {
+      asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;\n" ::
+                       : "memory");
+    }
     if (pl + 1 < pl_end) fetch(pl + 1);
     // the previous plane's bulk store must have read the exchange line before
     // this plane's first exit is published (after the first pass's barrier)
@@ -369,9 +386,14 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
       __syncthreads();
     };
 
-    // ---- between passes: record exits, place the next entries
-    // after the ascending pass of iteration it: y_it at segment ends, E_R(it)
-    // after the descending pass (it < K): x_it at segment starts, E_L(it+1)
+    // ---- between passes: one thread per segment takes the state handed to
+    // the zone (y_it at the end after an ascending pass, x_it at the start
+    // after a descending one), adds its response to the entries of the coming
+    // iterations (independent FMAs; each entry sums its terms in iteration
+    // order, as rf1_entry_left/right do), and places the entry of the next
+    // pass in the land slot. (Doing this in the thread that owns the exit
+    // point saves the barrier before it but costs 15 % more instructions in
+    // divergent warps: measured equal, 2.06 / 3.06 ms per 20-level x / y sweep.)
     auto boundary = [&](bool after_asc, int it) {
       const int SC = C * segcap;
       for (int w = tid; w < SC; w += NT) {
@@ -379,23 +401,24 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
         if (s >= scnt[cc]) continue;
         const int2 sg = sseg[w];
         const int i0 = sg.x, j0 = sg.x + sg.y - 1;
-        if (after_asc) {
-          hist[(K + it - 1) * SC + w] = sd[j0 * C + cc];
-          if (j0 < n - 1) {
-            double e = 0.0;
-            for (int j = 1; j <= it; ++j)
-              e = fma(zc[(K + it - j) * SC + w], hist[(K + j - 1) * SC + w], e);
-            if (TR) e *= __ldg(&a.c1[(line0 + cc) * gsl + j0 * gsp].x);
-            sd[(j0 + 1) * C + cc] = e;
+        if (after_asc) {  // entries E_R(k), k = it..K, live in acc[K + k - 1]
+          const double y = sd[j0 * C + cc];
+          double e = 0.0;
+          for (int k = it; k <= K; ++k) {
+            const double prev = it == 1 ? 0.0 : acc[(K + k - 1) * SC + w];
+            const double nv = fma(zc[(K + k - it) * SC + w], y, prev);
+            if (k == it) e = nv; else acc[(K + k - 1) * SC + w] = nv;
           }
-        } else {
-          hist[(it - 1) * SC + w] = sd[i0 * C + cc];
-          if (i0 > 0) {
-            double e = 0.0;
-            for (int j = 1; j <= it; ++j) e = fma(zc[(it + 1 - j) * SC + w], hist[(j - 1) * SC + w], e);
-            if (TR) e *= __ldg(&a.c1[(line0 + cc) * gsl + i0 * gsp].x);
-            sd[(i0 - 1) * C + cc] = e;
+          if (j0 < n - 1) sd[(j0 + 1) * C + cc] = TR ? e * salpha[SC + w] : e;
+        } else {          // entries E_L(k), k = it+1..K, live in acc[k - 1]
+          const double x = sd[i0 * C + cc];
+          double e = 0.0;
+          for (int k = it + 1; k <= K; ++k) {
+            const double prev = it == 1 ? 0.0 : acc[(k - 1) * SC + w];
+            const double nv = fma(zc[(k - it) * SC + w], x, prev);
+            if (k == it + 1) e = nv; else acc[(k - 1) * SC + w] = nv;
           }
+          if (i0 > 0) sd[(i0 - 1) * C + cc] = TR ? e * salpha[w] : e;
         }
       }
       __syncthreads();
@@ -471,8 +494,24 @@ bool rf1_res_launch_shape(const T* in, T* out, const Rf1LineArgs& a, cudaStream_
   const int64_t planes = a.nvar * a.nlev;
   const int64_t tiles = (nl + C - 1) / C;
   const int64_t groups = (planes + a.planes_per_cta - 1) / a.planes_per_cta;
-  kern<<<static_cast<unsigned>(tiles * groups), NT, smem, st>>>(in, out, a);
-  return true;
+  if (C == 1) {
+    kern<<<static_cast<unsigned>(tiles * groups), NT, smem, st>>>(in, out, a);
+    return true;
+  }
+  // clusters of two CTAs = two neighbouring tiles (an odd last tile gets an idle partner)
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(static_cast<unsigned>((tiles + 1) / 2 * groups * 2));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, in, out, a) == cudaSuccess;
 }
 
 template <typename T, bool TR>
