@@ -481,7 +481,7 @@ template <typename T, bool TR, int NT, int V, int C, int MINB>
 bool rf1_res_launch_shape(const T* in, T* out, const Rf1LineArgs& a, cudaStream_t st) {
   using L = Rf1ResSmem<NT, V, C>;
   const size_t smem = L::bytes(a.k, a.segcap);
-  if (smem > size_t(227) * 1024 / MINB) return false;
+  if (smem > size_t(227) * 1024) return false;  // MINB is a register hint; more smem only lowers occupancy
   auto kern = k_rf1_res<T, TR, NT, V, C, MINB>;
   static size_t attr = 0;
   if (smem > attr) {

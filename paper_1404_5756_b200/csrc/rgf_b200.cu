@@ -90,13 +90,22 @@ struct DevBuf {
   // kernels in flight on a non-blocking stream (e.g. the checkpoint buffer of
   // a transposed x sweep while the y sweep re-sizes it), and cudaFree does
   // not wait for those: drain the device first (rare: growth only).
+  bool owned = true;
   void release() {
-    if (p) {
+    if (p && owned) {
       cudaDeviceSynchronize();
       cudaFree(p);
     }
     p = nullptr;
     n = 0;
+    owned = true;
+  }
+  // a view of memory owned elsewhere (never freed here)
+  void borrow(T* ptr, size_t count) {
+    release();
+    p = ptr;
+    n = count;
+    owned = false;
   }
   void alloc(size_t count) {
     if (count <= n && p) return;
@@ -184,6 +193,8 @@ struct rgf_op {
   // planes): default on; RGF_B200_XT=0 at creation turns it off
   bool xt_mode = true;
   bool rf1_ok = false;  // streaming 1st-RF (ghost zones as per-segment convolutions)
+  DevBuf<double> cg_aux;      // dot partials, observation-space temporaries, one field (Cg)
+  DevBuf<double> cg_work;     // CG vectors of rgf_solve (b, chi, r, p, Ap, t, background, misfit)
   DevBuf<uint8_t> mask_same;  // per level: mask and ghost width equal the previous level's
   bool rf1_stream = true;  // streaming passes usable (every level has ghosts)
   bool rf1_line = true;  // line-resident 1st-RF sweeps (RGF_B200_RF1LINE=0 at creation: streaming)
@@ -849,6 +860,7 @@ struct rgf_obs {
   int64_t ncell = 0;
   DevBuf<int64_t> tcells, tptr;
   DevBuf<int32_t> tent;
+  DevBuf<char> arena;  // one allocation and one upload for all of the above
 };
 
 namespace {
@@ -880,10 +892,21 @@ struct Cg {
   int64_t nh;
   DevBuf<double> partial, scal, tmp_obs, tmp_obs2, tmp_f;
   void init() {
+    const size_t nobs = static_cast<size_t>(std::max<int64_t>(o->n, 1));
+    if (op) {  // the operator keeps these between calls (no cudaMalloc/cudaFree per solve)
+      op->cg_aux.alloc(rgfb::kDotBlocks + 1 + 2 * nobs + static_cast<size_t>(nh));
+      double* q = op->cg_aux.p;
+      partial.borrow(q, rgfb::kDotBlocks);
+      scal.borrow(q + rgfb::kDotBlocks, 1);
+      tmp_obs.borrow(q + rgfb::kDotBlocks + 1, nobs);
+      tmp_obs2.borrow(q + rgfb::kDotBlocks + 1 + nobs, nobs);
+      tmp_f.borrow(q + rgfb::kDotBlocks + 1 + 2 * nobs, static_cast<size_t>(nh));
+      return;
+    }
     partial.alloc(rgfb::kDotBlocks);
     scal.alloc(1);
-    tmp_obs.alloc(std::max<int64_t>(o->n, 1));
-    tmp_obs2.alloc(std::max<int64_t>(o->n, 1));
+    tmp_obs.alloc(nobs);
+    tmp_obs2.alloc(nobs);
     tmp_f.alloc(nh);
   }
   // a.b, or sum a^2 / r (r != nullptr)
@@ -1962,40 +1985,67 @@ int rgf_obs_create(const rgf_grid_desc* grid, int32_t device, int64_t n, const d
     }
     o->values_h.assign(values, values + n);
     o->rvar_h.assign(r_var, r_var + n);
-    // H^T gather lists in observation order (counting sort by cell)
-    const int64_t nh = grid->nx * grid->ny;
-    std::vector<int64_t> cnt(static_cast<size_t>(nh) + 1, 0);
+    // H^T gather lists: the touched cells in ascending order, each with its
+    // (observation, corner) entries in observation order. A stable sort of the
+    // 4n entries by cell (O(n log n); a counting sort over the nx*ny cells
+    // cost 10 ms per handle on a 1442x1021 grid).
     auto corner = [&](int64_t k, int q) {
       const int64_t c = cell[static_cast<size_t>(k)];
       return c + (q & 1) + (q >> 1) * grid->nx;
     };
+    // keys (cell, entry), sorted by cell with the entries of a cell in observation order
+    // (n < 2^29 entries fit 31 bits; cells < 2^33)
+    std::vector<uint64_t> ent(static_cast<size_t>(4 * n));
     for (int64_t k = 0; k < n; ++k)
-      for (int q = 0; q < 4; ++q) ++cnt[static_cast<size_t>(corner(k, q)) + 1];
+      for (int q = 0; q < 4; ++q)
+        ent[static_cast<size_t>(4 * k + q)] =
+            (static_cast<uint64_t>(corner(k, q)) << 31) | static_cast<uint64_t>(4 * k + q);
+    {  // LSD radix sort on the cell bits (stable; entries were generated in order)
+      const int64_t nh = grid->nx * grid->ny;
+      int bits = 1;
+      while ((int64_t(1) << bits) < nh) ++bits;
+      std::vector<uint64_t> tmp(ent.size());
+      for (int sh = 0; sh < bits; sh += 11) {
+        size_t cnt[2049] = {0};
+        for (uint64_t e : ent) ++cnt[((e >> (31 + sh)) & 2047u) + 1];
+        for (int b = 0; b < 2048; ++b) cnt[b + 1] += cnt[b];
+        for (uint64_t e : ent) tmp[cnt[(e >> (31 + sh)) & 2047u]++] = e;
+        ent.swap(tmp);
+      }
+    }
     std::vector<int64_t> tcells, tptr{0};
-    std::vector<int64_t> pos(static_cast<size_t>(nh), -1);
-    for (int64_t c = 0; c < nh; ++c)
-      if (cnt[static_cast<size_t>(c) + 1] > 0) {
-        pos[static_cast<size_t>(c)] = static_cast<int64_t>(tcells.size());
-        tcells.push_back(c);
-        tptr.push_back(tptr.back() + cnt[static_cast<size_t>(c) + 1]);
-      }
     std::vector<int32_t> tent(static_cast<size_t>(4 * n));
-    std::vector<int64_t> fill(tcells.size(), 0);
-    for (int64_t k = 0; k < n; ++k)
-      for (int q = 0; q < 4; ++q) {
-        const int64_t t = pos[static_cast<size_t>(corner(k, q))];
-        tent[static_cast<size_t>(tptr[static_cast<size_t>(t)] + fill[static_cast<size_t>(t)]++)] =
-            static_cast<int32_t>(4 * k + q);
+    for (size_t e = 0; e < ent.size(); ++e) {
+      const int64_t c = static_cast<int64_t>(ent[e] >> 31);
+      if (e == 0 || c != static_cast<int64_t>(ent[e - 1] >> 31)) {
+        if (e > 0) tptr.push_back(static_cast<int64_t>(e));
+        tcells.push_back(c);
       }
+      tent[e] = static_cast<int32_t>(ent[e] & 0x7fffffffu);
+    }
+    if (!ent.empty()) tptr.push_back(static_cast<int64_t>(ent.size()));
     o->ncell = static_cast<int64_t>(tcells.size());
-    if (n > 0) {
-      o->cell.upload(cell.data(), cell.size());
-      o->w.upload(w.data(), w.size());
-      o->values.upload(values, static_cast<size_t>(n));
-      o->rvar.upload(r_var, static_cast<size_t>(n));
-      o->tcells.upload(tcells.data(), tcells.size());
-      o->tptr.upload(tptr.data(), tptr.size());
-      o->tent.upload(tent.data(), tent.size());
+    if (n > 0) {  // one device allocation and one copy (seven cudaMallocs cost milliseconds)
+      const size_t sizes[7] = {cell.size() * sizeof(int64_t), w.size() * sizeof(double4),
+                               static_cast<size_t>(n) * sizeof(double),
+                               static_cast<size_t>(n) * sizeof(double),
+                               tcells.size() * sizeof(int64_t), tptr.size() * sizeof(int64_t),
+                               tent.size() * sizeof(int32_t)};
+      const void* srcs[7] = {cell.data(), w.data(), values, r_var, tcells.data(), tptr.data(),
+                             tent.data()};
+      size_t off[8] = {0};
+      for (int q = 0; q < 7; ++q) off[q + 1] = (off[q] + sizes[q] + 255) / 256 * 256;
+      std::vector<char> host(off[7]);
+      for (int q = 0; q < 7; ++q) std::memcpy(host.data() + off[q], srcs[q], sizes[q]);
+      o->arena.upload(host.data(), host.size());
+      char* base = o->arena.p;
+      o->cell.borrow(reinterpret_cast<int64_t*>(base + off[0]), cell.size());
+      o->w.borrow(reinterpret_cast<double4*>(base + off[1]), w.size());
+      o->values.borrow(reinterpret_cast<double*>(base + off[2]), static_cast<size_t>(n));
+      o->rvar.borrow(reinterpret_cast<double*>(base + off[3]), static_cast<size_t>(n));
+      o->tcells.borrow(reinterpret_cast<int64_t*>(base + off[4]), tcells.size());
+      o->tptr.borrow(reinterpret_cast<int64_t*>(base + off[5]), tptr.size());
+      o->tent.borrow(reinterpret_cast<int32_t*>(base + off[6]), tent.size());
     }
     *out = o.release();
   });
@@ -2109,9 +2159,17 @@ int rgf_solve(rgf_op* op, rgf_obs* o, double tol, int32_t max_iter, const double
     const int64_t nh = cg.nh, n = o->n;
     *out = rgf_analysis{};
     std::fill(increment, increment + nh, 0.0);
-    DevBuf<double> bg, d;
-    d.alloc(std::max<int64_t>(n, 1));
-    if (background) bg.upload(background, static_cast<size_t>(nh));
+    // CG work vectors live in the operator (grown on demand, reused by every
+    // solve: cudaMalloc/cudaFree of seven fields cost more than the iterations)
+    op->cg_work.alloc(static_cast<size_t>(7 * nh + std::max<int64_t>(n, 1)));
+    struct View {
+      double* p;
+    };
+    double* const w0 = op->cg_work.p;
+    View bg{w0}, b{w0 + nh}, chi{w0 + 2 * nh}, r{w0 + 3 * nh}, p{w0 + 4 * nh}, ap{w0 + 5 * nh},
+        t{w0 + 6 * nh}, d{w0 + 7 * nh};
+    if (background)
+      CUDA_OK(cudaMemcpy(bg.p, background, nh * sizeof(double), cudaMemcpyHostToDevice));
     cg.misfit(background ? bg.p : nullptr, d.p);
     if (n > 0 && misfit)
       CUDA_OK(cudaMemcpy(misfit, d.p, n * sizeof(double), cudaMemcpyDeviceToHost));
@@ -2119,8 +2177,6 @@ int rgf_solve(rgf_op* op, rgf_obs* o, double tol, int32_t max_iter, const double
       out->converged = 1;
       return;
     }
-    DevBuf<double> b, chi, r, p, ap, t;
-    for (DevBuf<double>* v : {&b, &chi, &r, &p, &ap, &t}) v->alloc(nh);
     const int blk = blocks_for(nh);
     cg.adjoint_rhs(d.p, b.p);
     const double bnorm = std::sqrt(cg.dot(b.p, b.p, nh));
