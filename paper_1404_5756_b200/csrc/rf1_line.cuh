@@ -298,9 +298,11 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
       }
     }
     __syncthreads();  // the staging buffer is free
-    if constexpr (C > 1) {
-      asm volatile("barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;\n" ::
-                       : "memory");
+    if constexpr (C > 1) {  // short lines: re-align the pair every 4th plane only
+      if (NT >= 256 || ((pl - pl_begin) & 3) == 0)
+        asm volatile(
+            "barrier.cluster.arrive.release.aligned;\n barrier.cluster.wait.acquire.aligned;\n" ::
+                : "memory");
     }
     if (pl + 1 < pl_end) fetch(pl + 1);
     // the previous plane's bulk store must have read the exchange line before
