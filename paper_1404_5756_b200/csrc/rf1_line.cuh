@@ -62,6 +62,7 @@ struct Rf1LineArgs {
   const double* post_scale; // output multiplier or null
   int segcap;               // max segments per line of this direction
   int planes_per_cta;       // planes a CTA walks through
+  int tma;                  // y tiles move by tensor copies (maps valid)
 };
 
 // 64 mask bits of a line starting at bit `start` (>= 0); bits past the packed
@@ -128,13 +129,15 @@ struct Rf1ResSmem {
 // points [q*V, q*V + V) of line c in registers.
 template <typename T, bool TR, int NT, int V, int C, int MINB>
 __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, T* __restrict__ out,
-                                                      Rf1LineArgs a) {
+                                                      Rf1LineArgs a,
+                                                      const __grid_constant__ CUtensorMap tm_in,
+                                                      const __grid_constant__ CUtensorMap tm_out) {
   using L = Rf1ResSmem<NT, V, C>;
   constexpr int CAP = L::CAP, NW = L::NW;
   constexpr int QW = 32 / C;          // chunks of one line per warp
   constexpr bool XD = C == 1;         // lines are rows of the field
   static_assert(32 % C == 0 && V <= 30, "shape");
-  extern __shared__ __align__(16) unsigned char smraw[];
+  extern __shared__ __align__(128) unsigned char smraw[];
   const int K = a.k, segcap = a.segcap;
   double* const sd = reinterpret_cast<double*>(smraw);  // exchange lines [p][C]; output staging
   T* const stg = reinterpret_cast<T*>(sd + CAP * C);    // input staging [p][C] (next plane)
@@ -183,6 +186,12 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
   const bool vec8 = !XD && sizeof(T) == 4 && C == 2 && nl % 2 == 0 && line0 + C <= nl &&
                     ((reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 8 == 0);
 
+  // y tiles as tensor copies: boxes of NQ rows x C columns (one thread issues them)
+  const bool tma = !XD && a.tma != 0;
+  constexpr int BR = L::NQ;
+  const int nbox = (n + BR - 1) / BR;
+  const bool abar = bulk || tma;  // arrivals counted on the mbarrier
+
   const int64_t pl_begin = grp * a.planes_per_cta;
   const int64_t pl_end = pl_begin + a.planes_per_cta < planes ? pl_begin + a.planes_per_cta : planes;
 
@@ -192,6 +201,15 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
       if (tid == 0) {
         mbar_arrive_expect_tx(bar, rowbytes);
         bulk_g2s(stg, src, rowbytes, bar);
+      }
+      return;
+    }
+    if (tma) {
+      if (tid == 0) {
+        const uint64_t pol = l2_evict_normal();
+        mbar_arrive_expect_tx(bar, static_cast<uint32_t>(nbox) * BR * C * sizeof(T));
+        for (int b = 0; b < nbox; ++b)
+          tma_load_3d(stg + b * BR * C, &tm_in, line0, b * BR, static_cast<int>(pl), bar, pol);
       }
       return;
     }
@@ -284,7 +302,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
     }
 
     // ---- this plane's lines: staging -> registers (land = 0, adjoint input scaling)
-    if (bulk) {
+    if (abar) {
       mbar_wait(bar, phase);
       phase ^= 1u;
     } else {
@@ -314,7 +332,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
     if (pl + 1 < pl_end) fetch(pl + 1);
     // the previous plane's bulk store must have read the exchange line before
     // this plane's first exit is published (after the first pass's barrier)
-    if (bulk && tid == 0) bulk_wait_read_all();
+    if (abar && tid == 0) bulk_wait_read_all();
 
     // ---- one pass
     auto pass = [&](auto asc_c, auto first_c, auto last_c, auto pull_c) {
@@ -463,6 +481,15 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
           bulk_s2g(dst, ost, rowbytes);
           bulk_commit();
         }
+      } else if (tma) {
+        fence_proxy_async_smem();
+        __syncthreads();
+        if (tid == 0) {
+          const uint64_t pol = l2_evict_normal();
+          for (int b = 0; b < nbox; ++b)
+            tma_store_3d(&tm_out, line0, b * BR, static_cast<int>(pl), ost + b * BR * C, pol);
+          bulk_commit();
+        }
       } else {
         __syncthreads();
         if (vec) {
@@ -485,7 +512,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
       }
     }
   }
-  if (bulk && tid == 0) bulk_wait_all();
+  if (abar && tid == 0) bulk_wait_all();
 }
 
 // ------------------------------------------------------------- launcher
@@ -506,9 +533,24 @@ bool rf1_res_launch_shape(const T* in, T* out, const Rf1LineArgs& a, cudaStream_
   const int64_t planes = a.nvar * a.nlev;
   const int64_t tiles = (nl + C - 1) / C;
   const int64_t groups = (planes + a.planes_per_cta - 1) / a.planes_per_cta;
+  CUtensorMap tmi{}, tmo{};
   if (C == 1) {
-    kern<<<static_cast<unsigned>(tiles * groups), NT, smem, st>>>(in, out, a);
+    kern<<<static_cast<unsigned>(tiles * groups), NT, smem, st>>>(in, out, a, tmi, tmo);
     return true;
+  }
+  Rf1LineArgs b = a;
+  b.tma = 0;
+  if (C * sizeof(T) >= 16 && (a.nx * sizeof(T)) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16 == 0) {
+    // field as a [planes][ny][nx] tensor; a tile's boxes are NQ rows x C columns
+    const uint64_t dims[3] = {static_cast<uint64_t>(a.nx), static_cast<uint64_t>(a.ny),
+                              static_cast<uint64_t>(planes)};
+    const uint64_t strides[2] = {static_cast<uint64_t>(a.nx) * sizeof(T),
+                                 static_cast<uint64_t>(a.nx) * a.ny * sizeof(T)};
+    const uint32_t box[3] = {static_cast<uint32_t>(C), static_cast<uint32_t>(NT / C), 1u};
+    tmi = make_tmap(in, tma_dtype<T>(), 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    tmo = make_tmap(out, tma_dtype<T>(), 3, dims, strides, box, CU_TENSOR_MAP_SWIZZLE_NONE);
+    b.tma = 1;
   }
   // clusters of CL CTAs = CL neighbouring tiles (a short last cluster gets idle partners)
   constexpr int CL = 2;
@@ -524,7 +566,7 @@ bool rf1_res_launch_shape(const T* in, T* out, const Rf1LineArgs& a, cudaStream_
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, in, out, a) == cudaSuccess;
+  return cudaLaunchKernelEx(&cfg, kern, in, out, b, tmi, tmo) == cudaSuccess;
 }
 
 template <typename T, bool TR>
