@@ -569,6 +569,21 @@ bool rf1_res_launch_shape(const T* in, T* out, const Rf1LineArgs& a, cudaStream_
   return cudaLaunchKernelEx(&cfg, kern, in, out, b, tmi, tmo) == cudaSuccess;
 }
 
+// y sweeps: tiles of CY adjacent columns, up to 2176 rows
+template <typename T, bool TR, int CY>
+bool launch_rf1_cols(const T* in, T* out, Rf1LineArgs a, cudaStream_t st) {
+  constexpr int W = CY / 2;  // thread-count factor of the 4-column shapes
+  const int64_t planes = a.nvar * a.nlev;
+  const int64_t n = a.ny, tiles = (a.nx + CY - 1) / CY;
+  int ppc = static_cast<int>(std::max<int64_t>(1, tiles * planes / (148 * 4 * 2)));
+  a.planes_per_cta = static_cast<int>(std::min<int64_t>(std::min<int64_t>(ppc, 16), planes));
+  if (n <= 32 * 9) return rf1_res_launch_shape<T, TR, 64 * W, 9, CY, 4>(in, out, a, st);
+  if (n <= 64 * 9) return rf1_res_launch_shape<T, TR, 128 * W, 9, CY, 4 / W>(in, out, a, st);
+  if (n <= 64 * 17) return rf1_res_launch_shape<T, TR, 128 * W, 17, CY, 4 / W>(in, out, a, st);
+  if (n <= 128 * 17) return rf1_res_launch_shape<T, TR, 256 * W, 17, CY, 2 / W>(in, out, a, st);
+  return false;
+}
+
 template <typename T, bool TR>
 bool launch_rf1_line_tr(const T* in, T* out, Rf1LineArgs a, cudaStream_t st) {
   const int64_t planes = a.nvar * a.nlev;
@@ -583,19 +598,16 @@ bool launch_rf1_line_tr(const T* in, T* out, Rf1LineArgs a, cudaStream_t st) {
     return false;
   }
   // columns: tiles of 2 adjacent columns (16 B row pieces in fp64; the other
-  // half of each 32 B sector belongs to the neighbouring tile, whose CTA runs
-  // in the same wave), up to 2176 rows. Measured on C5 (20 levels, fp64 y
-  // sweep): 2 columns x 256 threads, two CTAs per SM 2.93 ms; 4 columns x 512
-  // threads, one CTA per SM 3.20 ms.
-  constexpr int CY = 2;
-  const int64_t n = a.ny, tiles = (a.nx + CY - 1) / CY;
-  int ppc = static_cast<int>(std::max<int64_t>(1, tiles * planes / (148 * 4 * 2)));
-  a.planes_per_cta = static_cast<int>(std::min<int64_t>(std::min<int64_t>(ppc, 16), planes));
-  if (n <= 32 * 9) return rf1_res_launch_shape<T, TR, 64, 9, CY, 4>(in, out, a, st);
-  if (n <= 64 * 9) return rf1_res_launch_shape<T, TR, 128, 9, CY, 4>(in, out, a, st);
-  if (n <= 64 * 17) return rf1_res_launch_shape<T, TR, 128, 17, CY, 4>(in, out, a, st);
-  if (n <= 128 * 17) return rf1_res_launch_shape<T, TR, 256, 17, CY, 2>(in, out, a, st);
-  return false;
+  // half of each 32 B sector belongs to the neighbouring tile of the cluster).
+  // Measured on C5 (20 levels, fp64 y sweep, cp.async pieces): 2 columns x 256
+  // threads, two CTAs per SM 2.93 ms; 4 columns x 512 threads, one CTA per SM
+  // 3.20 ms. fp32 fields whose rows allow tensor copies take 4-column tiles
+  // (16 B pieces; C5 fp32 y sweep 15.7 -> 14.3 ms), others 2-column tiles
+  // with 8 B cp.async pieces.
+  if (sizeof(T) == 4 && (a.nx * sizeof(T)) % 16 == 0 &&
+      (reinterpret_cast<uintptr_t>(in) | reinterpret_cast<uintptr_t>(out)) % 16 == 0)
+    return launch_rf1_cols<T, TR, 4>(in, out, a, st);
+  return launch_rf1_cols<T, TR, 2>(in, out, a, st);
 }
 
 // One sweep (all K iterations) of direction a.dir; false when the line does
