@@ -525,8 +525,10 @@ bool rf1_res_launch_shape(const T* in, T* out, const Rf1LineArgs& a, cudaStream_
   static size_t attr = 0;
   if (smem > attr) {
     if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             static_cast<int>(smem)) != cudaSuccess)
+                             static_cast<int>(smem)) != cudaSuccess) {
+      (void)cudaGetLastError();
       return false;
+    }
     attr = smem;
   }
   const int64_t nl = C == 1 ? a.ny : a.nx;
@@ -566,7 +568,11 @@ bool rf1_res_launch_shape(const T* in, T* out, const Rf1LineArgs& a, cudaStream_
   at[0].val.clusterDim.z = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kern, in, out, b, tmi, tmo) == cudaSuccess;
+  if (cudaLaunchKernelEx(&cfg, kern, in, out, b, tmi, tmo) != cudaSuccess) {
+    (void)cudaGetLastError();  // the caller falls back to the streaming passes
+    return false;
+  }
+  return true;
 }
 
 // y sweeps: tiles of CY adjacent columns, up to 2176 rows
