@@ -241,6 +241,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
   uint32_t live = 0, starts = 0, ends = 0, slotL = 0, slotR = 0, seab = 0;
   double la[V];
   double A = 1.0;  // the chunk's link product
+  int my_i0 = 0, my_j0 = -1;
   uint32_t phase = 0;
   for (int64_t pl = pl_begin; pl < pl_end; ++pl) {
     const int64_t var = pl / a.nlev, lev = a.lev0 + (pl - var * a.nlev);
@@ -309,6 +310,17 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
       asm volatile("cp.async.wait_group 0;\n" ::: "memory");
     }
     __syncthreads();
+    if (!reuse) {  // this thread's first segment of the between-pass phase
+      my_j0 = -1;
+      if (tid < C * segcap) {
+        const int cc = tid / segcap, sgi = tid - cc * segcap;
+        if (sgi < scnt[cc]) {
+          const int2 sg = sseg[tid];
+          my_i0 = sg.x;
+          my_j0 = sg.x + sg.y - 1;
+        }
+      }
+    }
     double v[V];
     {
       const double* pre =
@@ -423,11 +435,7 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
     // divergent warps: measured equal, 2.06 / 3.06 ms per 20-level x / y sweep.)
     auto boundary = [&](bool after_asc, int it) {
       const int SC = C * segcap;
-      for (int w = tid; w < SC; w += NT) {
-        const int cc = w / segcap, s = w - cc * segcap;
-        if (s >= scnt[cc]) continue;
-        const int2 sg = sseg[w];
-        const int i0 = sg.x, j0 = sg.x + sg.y - 1;
+      auto serve = [&](int w, int cc, int i0, int j0) {
         if (after_asc) {  // entries E_R(k), k = it..K, live in acc[K + k - 1]
           const double y = sd[j0 * C + cc];
           double e = 0.0;
@@ -447,6 +455,15 @@ __global__ void __launch_bounds__(NT, MINB) k_rf1_res(const T* __restrict__ in, 
           }
           if (i0 > 0) sd[(i0 - 1) * C + cc] = TR ? e * salpha[w] : e;
         }
+      };
+      // the thread's first segment sits in registers (no lookups on the
+      // latency path between the two barriers); further ones come from the list
+      if (my_j0 >= 0) serve(tid, tid / segcap, my_i0, my_j0);
+      for (int w = tid + NT; w < SC; w += NT) {
+        const int cc = w / segcap, s = w - cc * segcap;
+        if (s >= scnt[cc]) continue;
+        const int2 sg = sseg[w];
+        serve(w, cc, sg.x, sg.x + sg.y - 1);
       }
       __syncthreads();
     };
